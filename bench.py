@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark of the wind-downscaling hot path (arXiv 2101.08453) on B200.
+
+One *step* = one pass of the whole hot path over the
+synthetic Paper-scale workload (BASELINE.json configs[3], 3000x3000x15
+elements, a = (1,1,10)):
+    wd_assemble (validate + 2x2x2-Gauss assembly + plan + Galerkin + coarsest
+    inverse) -> wd_rhs -> wd_solve (zero start, rel. residual 1e-8) ->
+    wd_recover_wind.
+metric: fine-grid nodes x V-cycles per second over the step (BASELINE metric),
+timed with CUDA events on the launching stream, inputs resident in HBM
+(larger than the 126 MB L2, so no flush is needed).  Extra keys report the
+time to 1e-8, the roofline of the dominant kernel (level-0 Gauss-Seidel
+phase), the oracle's CPU baseline, the end-to-end number through the C ABI
+with host buffers, clocks and the launch count.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config paper|medium|small|tiny]
+Under torchrun (N > 1) every rank solves its own copy of the workload
+(independent problems, no data-path collective: "scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_NAMES = {"tiny": "tiny 16x16x8 (configs[0])", "small": "small 128x128x10 (configs[1])",
+                "medium": "medium 1000x1000x15 (configs[2])",
+                "paper": "paper-scale 3000x3000x15 (configs[3])"}
+GS_BYTES_PER_FREE_NODE_PER_LAUNCH = 66   # 264 B/node/sweep over 4 phases
+CPU_CROP = 200                            # oracle sample: 200x200x15 elements of the workload
+
+
+def measured_hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler (200 ms) running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(ws, v):
+    if ws == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def make_problem(name, device):
+    import synth
+    return synth.make(name, device=device)
+
+
+# ---------------------------------------------------------------- oracle arm
+def oracle_step(prob_cpu, tol):
+    """One oracle pass (as it stands) over the bounded CPU sample."""
+    import oracle
+    X, Y, Z, u0 = prob_cpu.numpy()
+    t0 = time.perf_counter()
+    mg = oracle.MG(X, Y, Z, prob_cpu.a)
+    f = oracle.rhs(X, Y, Z, u0)
+    lam, rep = mg.solve(f, tol=tol, max_cycles=100)
+    oracle.recover(X, Y, Z, prob_cpu.a, lam, u0)
+    dt = time.perf_counter() - t0
+    del mg
+    return dt, rep["cycles"], rep
+
+
+def cpu_sample(prob):
+    import synth
+    m = min(CPU_CROP, prob.nx)
+    return synth.crop(prob, (prob.nx - m) // 2, (prob.ny - m) // 2, m, m).to("cpu")
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    import oracle
+    prob = make_problem(args.config, "cuda" if torch.cuda.is_available() else "cpu")
+    samp = cpu_sample(prob)
+    del prob
+    nodes = samp.n_nodes
+    for _ in range(args.warmup):
+        oracle_step(samp, args.tol)
+    tot, cyc = 0.0, 0
+    for _ in range(args.steps):
+        dt, c, rep = oracle_step(samp, args.tol)
+        tot += dt
+        cyc += c
+    value = nodes * cyc / tot
+    cores = oracle.num_threads()
+    sample = (f"{samp.nx}x{samp.ny}x{samp.nz}-element centre crop of the {args.config} workload "
+              f"({nodes} nodes), full step (assemble+rhs+solve to {args.tol:g}+recover)")
+    line = {"impl": "reference", "metric": "fine node-V-cycles/s", "value": value,
+            "unit": "node-cycles/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[args.config], "sample": sample,
+                       "rel_tol": args.tol},
+            "cycles_per_step": cyc / args.steps, "rate": rep["rate"],
+            "cpu_baseline": {"value": value, "unit": "node-cycles/s", "cores": cores,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "node-cycles/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def gpu_step(wd, prob, opt, tol, stream, host=None):
+    """One full step through the C ABI.  host: dict of pinned host tensors for
+    the end-to-end variant (inputs copied in, lambda and u copied out)."""
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev[0].record(stream)
+    if host is None:
+        ctx = wd.wd_assemble(prob.X, prob.Y, prob.Z, prob.a, opt)
+        ev[1].record(stream)
+        f = wd.wd_rhs(ctx, prob.u0)
+        ev[2].record(stream)
+        lam, rep = wd.wd_solve(ctx, f, rel_tol=tol, raise_on_noconv=False)
+        ev[3].record(stream)
+        u = wd.wd_recover_wind(ctx, lam, prob.u0)
+    else:
+        ctx = wd.wd_assemble(host["X"], host["Y"], host["Z"], prob.a, opt)
+        ev[1].record(stream)
+        f = torch.empty(ctx.node_shape, dtype=torch.float64, device="cuda")
+        wd.wd_rhs(ctx, host["u0"], f)
+        ev[2].record(stream)
+        _, rep = wd.wd_solve(ctx, f, rel_tol=tol, lam=host["lam"], raise_on_noconv=False)
+        ev[3].record(stream)
+        u = wd.wd_recover_wind(ctx, host["lam"], host["u0"], host["u"])
+    ev[4].record(stream)
+    prof = wd.wd_profile_read(ctx)
+    return ctx, ev, rep, prof, (f, u)
+
+
+def run_ours(args, ws, rank, local):
+    import paper_2101_08453_b200 as wd
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    prob = make_problem(args.config, dev)
+    opt = wd.default_options(profile=1, coarsen_rule=args.rule)
+    nodes = prob.n_nodes
+
+    def one(host=None):
+        ctx, ev, rep, prof, keep = gpu_step(wd, prob, opt, args.tol, stream, host)
+        return ctx, ev, rep, prof
+
+    # warm-up
+    for _ in range(args.warmup):
+        ctx, ev, rep, prof = one()
+        torch.cuda.synchronize()
+        levels = [ctx.level_dims(l) for l in range(ctx.num_levels())]
+        plans = [ctx.level_plan(l) for l in range(ctx.num_levels() - 1)]
+        dev_bytes = ctx.device_bytes()
+        ctx.close()
+    # timed region
+    barrier(ws)
+    torch.cuda.synchronize()
+    l0 = wd.wd_launch_count()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    parts = np.zeros(4)
+    cycles, gs_ms, gs_sweeps, vc_ms, vc_n, rates = 0, 0.0, 0, 0.0, 0, []
+    with Clocks(local) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            ctx, ev, rep, prof = one()
+            ev[4].synchronize()
+            parts += [ev[t].elapsed_time(ev[t + 1]) for t in range(4)]
+            cycles += rep["cycles"]
+            rates.append(rep["rate"])
+            gs_ms += prof["gs0_ms"]
+            gs_sweeps += int(prof["gs0_sweeps"])
+            vc_ms += prof["vcycle_ms"]
+            vc_n += int(prof["vcycles"])
+            ctx.close()   # frees device memory; ordered after the step's work
+        stop.record(stream)
+        torch.cuda.synchronize()
+    launches = wd.wd_launch_count() - l0
+    barrier(ws)
+    ms_total = max_over_ranks(ws, start.elapsed_time(stop))
+    ms_step = ms_total / args.steps
+    value = ws * nodes * (cycles / args.steps) / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel: one colour phase of the level-0 smoother
+    peak, peak_src = measured_hbm_peak()
+    n1, n2, n3 = prob.dims
+    free0 = (n1 - 2) * (n2 - 2) * (n3 - 1)
+    launch_ms = gs_ms / max(gs_sweeps, 1) / 4.0
+    bytes_launch = GS_BYTES_PER_FREE_NODE_PER_LAUNCH * free0
+    achieved = bytes_launch / (launch_ms * 1e-3) / 1e9 if launch_ms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_gs_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.config)
+        except Exception:
+            traffic = None
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": "fine node-V-cycles/s", "value": value, "unit": "node-cycles/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[args.config], "nodes": nodes,
+                       "elements": prob.nx * prob.ny * prob.nz, "free_unknowns": free0,
+                       "a": list(prob.a), "rel_tol": args.tol, "coarsen_rule": args.rule,
+                       "levels": levels, "plans_horizontal": [p["horizontal"] for p in plans],
+                       "step": "wd_assemble + wd_rhs + wd_solve(zero start) + wd_recover_wind",
+                       "l2": "inputs larger than L2 (no flush)",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+            "cycles_per_step": cycles / args.steps, "rate": float(np.mean(rates)),
+            "time_to_1e-8_s": parts[2] / args.steps * 1e-3,
+            "breakdown_ms": {"assemble_setup": parts[0] / args.steps,
+                             "rhs": parts[1] / args.steps, "solve": parts[2] / args.steps,
+                             "recover": parts[3] / args.steps},
+            "ms_per_vcycle": vc_ms / max(vc_n, 1),
+            "device_bytes": dev_bytes,
+            "roofline": {"kernel": "gs_phase_kernel (level 0)", "bound": "hbm",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "bytes_per_launch": bytes_launch, "launch_ms": launch_ms,
+                         "peak_source": peak_src},
+            "gpu_launches": int(launches), "clocks": clk.summary(),
+        }
+    # end to end through the ABI with host (pinned) buffers
+    if not args.no_e2e:
+        host = {"X": prob.X.cpu().pin_memory(), "Y": prob.Y.cpu().pin_memory(),
+                "Z": prob.Z.cpu().pin_memory(), "u0": prob.u0.cpu().pin_memory()}
+        host["lam"] = torch.empty(prob.X.shape, dtype=torch.float64).pin_memory()
+        host["u"] = torch.empty(prob.u0.shape, dtype=torch.float64).pin_memory()
+        ctx, *_ = one(host)
+        torch.cuda.synchronize()
+        ctx.close()
+        ne = max(1, min(args.steps, 2))
+        barrier(ws)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ecyc = 0
+        s0.record(stream)
+        for _ in range(ne):
+            ctx, ev, rep, prof = one(host)
+            ecyc += rep["cycles"]
+            ctx.close()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        ems = max_over_ranks(ws, s0.elapsed_time(s1)) / ne
+        nb = 8 * nodes
+        ne_el = 8 * prob.nx * prob.ny * prob.nz * 3
+        if line is not None:
+            line["e2e"] = {"value": ws * nodes * (ecyc / ne) / (ems * 1e-3),
+                           "unit": "node-cycles/s", "ms_per_step": ems,
+                           "h2d_bytes_per_step": 3 * nb + 2 * ne_el + nb,
+                           "d2h_bytes_per_step": nb + ne_el,
+                           "note": "pinned host X,Y,Z,u0 in; lambda,u out; copies inside the ABI calls"}
+        del host
+    # oracle baseline on the host cores (rank 0, N = 1 only)
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        import oracle
+        samp = cpu_sample(prob)
+        tot, cyc, nst = 0.0, 0, 0
+        while tot < 10.0 and nst < 4:
+            dt, c, _ = oracle_step(samp, args.tol)
+            tot += dt
+            cyc += c
+            nst += 1
+        line["cpu_baseline"] = {
+            "value": samp.n_nodes * cyc / tot, "unit": "node-cycles/s",
+            "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": (f"{nst} full steps on the {samp.nx}x{samp.ny}x{samp.nz}-element centre "
+                       f"crop ({samp.n_nodes} nodes), {tot:.1f} s")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="paper", choices=list(CONFIG_NAMES))
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--rule", default="coupling_cur",
+                    choices=["coupling_cur", "coupling_paper", "verbatim", "full"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

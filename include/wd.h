@@ -1,0 +1,184 @@
+/*
+ * wd.h -- C ABI of the B200-native (sm_100a, fp64) mass-consistent wind
+ * downscaling library (Mandel, Farguell, Kochanski, Mallia, Hilburn,
+ * arXiv 2101.08453; "P:n" = /root/reference/PAPER.md line n).
+ *
+ * The library solves, on a terrain-following grid of isoparametric 8-node
+ * hexahedra, the generalised Poisson problem (Eq. (4))
+ *        -div A^{-1} grad lambda = div u0,  lambda = 0 on dOmega \ Gamma,
+ * in its variational form (Eq. (5)) with 2x2x2 Gauss quadrature on
+ * the left and one-point quadrature on the right, by a multigrid
+ * V-cycle (Eq. (6)-(7)), and recovers u = u0 + A^{-1} grad lambda
+ * at element centres (Eq. (3)).  A = diag(a1^2,a2^2,a3^2).
+ *
+ * Conventions for every array argument (all IEEE fp64, C-contiguous):
+ *   node arrays   [n3][n2][n1]       i fastest, node (i,j,k), n1 = nx + 1 ...
+ *                 (X, Y, Z, f, lambda, lambda0)
+ *   element arrays [3][n3-1][n2-1][n1-1]  SoA components u, v, w (u0, u)
+ *   Gamma (the terrain, natural boundary) is the k = 0 node plane; the
+ *   Dirichlet set D is i in {0, n1-1}, j in {0, n2-1}, k = n3-1.
+ * Pointers may be device pointers (cudaMalloc / torch CUDA tensors) or host
+ * pointers; host arrays are staged through device memory inside the call
+ * and the call then synchronises `stream` before returning.
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ * stream-ordered on it, except wd_assemble (synchronous) and wd_solve (which
+ * synchronises once per V-cycle to test convergence).
+ *
+ * Ownership: the caller owns every array passed in or out; the context owns
+ * only internal copies and workspaces, allocated by wd_assemble and freed by
+ * wd_destroy (wd_device_bytes reports their size).  A context is not
+ * thread-safe; use one per host thread / stream.
+ *
+ * Errors: every int-returning call returns WD_OK (0) or a WD_E_* code and
+ * never aborts; wd_last_error() returns a thread-local message for the last
+ * non-zero return of the calling thread.
+ */
+#ifndef WD_H
+#define WD_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    WD_OK = 0,
+    WD_E_INVAL = 1,     /* n1,n2 < 3; n3 < 2; NULL pointer; a_d <= 0 or non-finite; tol not in (0,1) */
+    WD_E_MESH = 2,      /* Z not increasing in k, or detJ <= 0 at a Gauss point (message names element) */
+    WD_E_NOCONV = 3,    /* max_cycles reached; lambda valid, report filled */
+    WD_E_DIVERGED = 4,  /* relative residual grew 10x over 3 consecutive cycles */
+    WD_E_NONFINITE = 5, /* residual norm became NaN/Inf */
+    WD_E_CUDA = 6,      /* CUDA runtime failure */
+    WD_E_NCCL = 7,      /* communicator failure (multi-GPU) */
+    WD_E_OOM = 8,       /* device allocation failed */
+    WD_E_INTERNAL = 9   /* planner/Galerkin invariant violated */
+};
+
+/* Semicoarsening rule of P:192-202 (readings C1/C1b of DESIGN.md):
+ *  COUPLING_CUR   ratio (h3/h1)(a3/a1), vertical test with the current-level h1 (default)
+ *  COUPLING_PAPER ratio (h3/h1)(a3/a1), vertical test with the coarsened h1 (P:196-199 literal)
+ *  VERBATIM       ratio h3/(h1 a3) exactly as printed, coarsened h1
+ *  FULL           base method: 2x2x2 coarsening at every level */
+enum { WD_RULE_COUPLING_CUR = 0, WD_RULE_COUPLING_PAPER = 1, WD_RULE_VERBATIM = 2, WD_RULE_FULL = 3 };
+
+typedef struct wd_ctx wd_ctx;
+
+typedef struct {
+    int pre_smooth;          /* GS sweeps before the coarse correction (default 2; "four smoothing steps") */
+    int post_smooth;         /* GS sweeps after it (default 2) */
+    int max_cycles;          /* wd_solve cycle cap (default 100) */
+    int coarsest_max_free;   /* direct coarsest solve at <= this many free unknowns (default 4096) */
+    int coarse_iters;        /* GS sweeps on the coarsest level when it is larger (default 50) */
+    int coarsen_rule;        /* WD_RULE_* (default WD_RULE_COUPLING_CUR) */
+    int use_graph;           /* capture the V-cycle as a CUDA graph (default 1) */
+    long long gather_below_nodes; /* multi-GPU coarse gather threshold (reserved, default 0) */
+    int rank, nranks;        /* multi-GPU slab decomposition (reserved; 0, 1 on one GPU) */
+    void* nccl_comm;         /* reserved, NULL */
+    int j_begin, j_end;      /* reserved: owned node rows [j_begin, j_end) */
+    int profile;             /* 1: CUDA events around level-0 smoothing and each V-cycle (default 0) */
+} wd_options;
+
+typedef struct {
+    int status;              /* WD_OK / WD_E_NOCONV / WD_E_DIVERGED / WD_E_NONFINITE */
+    int cycles;              /* V-cycles performed */
+    int converged;           /* rel_res_final <= tol */
+    int nlevels;             /* hierarchy depth (incl. the fine level) */
+    double rel_res0;         /* ||f - K lambda0|| / ||f|| over free nodes (abs if ||f|| = 0) */
+    double rel_res_final;
+    double rate;             /* (rel_N / rel_1)^(1/(N-1)); rel_1/rel_0 if N = 1 */
+    double rel_res_hist[256];/* [c] = relative residual after cycle c, [0] = initial */
+    int dims[32][3];         /* node dims (n1,n2,n3) per level */
+    int coarse_direct;       /* 1 dense direct coarsest solve, 0 GS fallback */
+    int coarse_free;         /* free unknowns on the coarsest level */
+} wd_report;
+
+/* Fill opt with the defaults above. */
+void wd_default_options(wd_options* opt);
+
+/* Setup once per mesh (P:107-111 assembly, P:151-158 + P:192-202 hierarchy).
+ * X, Y, Z: node coordinates [n3][n2][n1]; a1, a2, a3 > 0: penalty constants of
+ * A = diag(a1^2, a2^2, a3^2).  Validates the mesh (WD_E_MESH names
+ * the lowest failing element), assembles the 27-point operator (stored as 14
+ * symmetric coefficients per node), plans the coarsening, forms the Galerkin
+ * coarse operators and factors the coarsest level.  opt may be NULL
+ * (defaults).  Synchronous; the caller may free X, Y, Z on return.
+ * On success *out receives a new context. */
+int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
+                double a1, double a2, double a3, const wd_options* opt, void* stream,
+                wd_ctx** out);
+
+/* RHS of Eq. (5) by one-point quadrature:
+ * f_p = sum_{e ni p} -8 detJ_e(0) grad N_p(0) . u0_e, f = 0 on D.
+ * u0: element array; f: node array (written). */
+int wd_rhs(wd_ctx* ctx, const double* u0, double* f, void* stream);
+
+/* One multigrid V-cycle on lambda (in/out node array) for K lambda = f
+ * (Eq. (7)): pre-smoothing, f_c = P^T (f - K lambda), recursive
+ * coarse solve from 0, lambda += P lambda_c, post-smoothing.  lambda entries
+ * on D are treated as 0 and returned as 0.  rel_res_out (nullable, host)
+ * receives ||f - K lambda||/||f|| after the cycle (synchronises). */
+int wd_vcycle(wd_ctx* ctx, double* lambda, const double* f, double* rel_res_out, void* stream);
+
+/* Iterate V-cycles from lambda0 (NULL = zero start; entries on D ignored)
+ * until ||f - K lambda||/||f|| <= rel_tol (in (0,1)), max_cycles, divergence
+ * or a non-finite residual.  f = 0 returns lambda = 0 after 0 cycles.
+ * lambda (out) may alias lambda0.  rep (nullable, host) is filled.
+ * Returns WD_OK, WD_E_NOCONV, WD_E_DIVERGED or WD_E_NONFINITE (lambda is the
+ * last iterate in every case). */
+int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol,
+             double* lambda, wd_report* rep, void* stream);
+
+/* Wind recovery, Eq. (3) with grad lambda at element centres:
+ * u_e = u0_e + A^{-1} J_e(0)^{-T} sum_a lambda_a grad_xi N_a(0).
+ * lambda: node array; u0, u: element arrays (u may alias u0). */
+int wd_recover_wind(wd_ctx* ctx, const double* lambda, const double* u0, double* u,
+                    void* stream);
+
+/* Free the context and all its device memory (NULL is a no-op). */
+void wd_destroy(wd_ctx* ctx);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* wd_last_error(void);
+
+/* ---- inspection entry points (used by the parity tests; same conventions) ---- */
+
+/* Bytes of device memory owned by the context. */
+long long wd_device_bytes(const wd_ctx* ctx);
+/* Number of levels; node dims of level l (dims[3] = n1, n2, n3). */
+int wd_num_levels(const wd_ctx* ctx);
+int wd_level_dims(const wd_ctx* ctx, int level, int dims[3]);
+/* Plan of the transition level -> level+1: *horizontal, kept node layers. */
+int wd_level_plan(const wd_ctx* ctx, int level, int* horizontal, int* kept, int* nkept);
+/* Full 27-point stencil of level l as [n3][n2][n1][27] (o = (dx+1)+3(dy+1)+9(dz+1)),
+ * both directions of each symmetric coupling (device or host output). */
+int wd_get_stencil(wd_ctx* ctx, int level, double* K27, void* stream);
+/* y = K_l x on free nodes, 0 on D (node arrays of level l). */
+int wd_apply(wd_ctx* ctx, int level, const double* x, double* y, void* stream);
+/* `sweeps` 4-colour bottom-up Gauss-Seidel sweeps on level l. */
+int wd_smooth(wd_ctx* ctx, int level, double* x, const double* f, int sweeps, void* stream);
+/* fc = P^T r from level l to level l+1 (r treated as 0 on D). */
+int wd_restrict(wd_ctx* ctx, int level, const double* r, double* fc, void* stream);
+/* x += P xc from level l+1 to level l on free nodes. */
+int wd_prolong(wd_ctx* ctx, int level, const double* xc, double* x, void* stream);
+/* Coarsest-level solve x = K_L^{-1} f (or the GS fallback), node arrays of the last level. */
+int wd_coarse_solve(wd_ctx* ctx, const double* f, double* x, void* stream);
+/* ||f - K x||_2 over free nodes of level 0 and its ratio to ||f||_2 (host outputs). */
+int wd_residual_norm(wd_ctx* ctx, const double* x, const double* f, double* abs_out,
+                     double* rel_out, void* stream);
+
+/* Device-side profile gathered while opt.profile = 1 (CUDA events, also inside
+ * the captured V-cycle graph), accumulated over wd_solve/wd_vcycle calls:
+ *   out[0] ms in level-0 GS sweeps   out[1] level-0 sweeps (4 launches each)
+ *   out[2] ms in V-cycles             out[3] V-cycles
+ *   out[4] ms in residual-norm passes out[5] residual-norm passes
+ * Returns the number of values written (<= n). */
+int wd_profile_read(const wd_ctx* ctx, double* out, int n);
+/* Reset the accumulated profile. */
+void wd_profile_reset(wd_ctx* ctx);
+/* Cumulative number of kernel launches executed by this library in this
+ * process (a CUDA-graph replay counts its kernel nodes). */
+long long wd_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WD_H */

@@ -1,0 +1,298 @@
+"""Python binding of the B200-native wind-downscaling library (``libwd.so``).
+
+Argument marshalling only: every function forwards to the C ABI declared in
+``include/wd.h`` (same names), passing raw pointers of torch tensors (device or
+host) and the current CUDA stream.  All arithmetic of the hot path runs in the
+sm_100a kernels of ``csrc/``; there is no CPU or PyTorch fallback -- importing
+this package fails loudly if the shared library is missing.
+
+Paper: Mandel et al., arXiv 2101.08453 (Eq. (3)-(7), Sec. 3).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwd.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `make` or __graft_entry__.build() "
+                      "(the CUDA extension is required; there is no fallback)")
+
+_lib = C.CDLL(LIB_PATH)
+
+WD_OK, WD_E_INVAL, WD_E_MESH, WD_E_NOCONV, WD_E_DIVERGED, WD_E_NONFINITE, WD_E_CUDA, \
+    WD_E_NCCL, WD_E_OOM, WD_E_INTERNAL = range(10)
+RULES = {"coupling_cur": 0, "coupling_paper": 1, "verbatim": 2, "full": 3}
+ERRNAMES = {1: "WD_E_INVAL", 2: "WD_E_MESH", 3: "WD_E_NOCONV", 4: "WD_E_DIVERGED",
+            5: "WD_E_NONFINITE", 6: "WD_E_CUDA", 7: "WD_E_NCCL", 8: "WD_E_OOM",
+            9: "WD_E_INTERNAL"}
+
+
+class wd_options(C.Structure):
+    _fields_ = [("pre_smooth", C.c_int), ("post_smooth", C.c_int), ("max_cycles", C.c_int),
+                ("coarsest_max_free", C.c_int), ("coarse_iters", C.c_int),
+                ("coarsen_rule", C.c_int), ("use_graph", C.c_int),
+                ("gather_below_nodes", C.c_longlong), ("rank", C.c_int), ("nranks", C.c_int),
+                ("nccl_comm", C.c_void_p), ("j_begin", C.c_int), ("j_end", C.c_int),
+                ("profile", C.c_int)]
+
+
+class wd_report(C.Structure):
+    _fields_ = [("status", C.c_int), ("cycles", C.c_int), ("converged", C.c_int),
+                ("nlevels", C.c_int), ("rel_res0", C.c_double), ("rel_res_final", C.c_double),
+                ("rate", C.c_double), ("rel_res_hist", C.c_double * 256),
+                ("dims", (C.c_int * 3) * 32), ("coarse_direct", C.c_int),
+                ("coarse_free", C.c_int)]
+
+    def to_dict(self):
+        c = self.cycles
+        return dict(status=self.status, cycles=c, converged=bool(self.converged),
+                    nlevels=self.nlevels, rel_res0=self.rel_res0,
+                    rel_res_final=self.rel_res_final, rate=self.rate,
+                    hist=[self.rel_res_hist[t] for t in range(min(c, 255) + 1)],
+                    dims=[tuple(self.dims[l]) for l in range(self.nlevels)],
+                    coarse_direct=bool(self.coarse_direct), coarse_free=self.coarse_free)
+
+
+_vp = C.c_void_p
+_dp = C.c_void_p
+_lib.wd_default_options.argtypes = [C.POINTER(wd_options)]
+_lib.wd_last_error.restype = C.c_char_p
+_lib.wd_assemble.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                             C.c_double, C.POINTER(wd_options), _vp, C.POINTER(_vp)]
+_lib.wd_rhs.argtypes = [_vp, _dp, _dp, _vp]
+_lib.wd_vcycle.argtypes = [_vp, _dp, _dp, C.POINTER(C.c_double), _vp]
+_lib.wd_solve.argtypes = [_vp, _dp, _dp, C.c_double, _dp, C.POINTER(wd_report), _vp]
+_lib.wd_recover_wind.argtypes = [_vp, _dp, _dp, _dp, _vp]
+_lib.wd_destroy.argtypes = [_vp]
+_lib.wd_device_bytes.argtypes = [_vp]
+_lib.wd_device_bytes.restype = C.c_longlong
+_lib.wd_num_levels.argtypes = [_vp]
+_lib.wd_level_dims.argtypes = [_vp, C.c_int, C.POINTER(C.c_int)]
+_lib.wd_level_plan.argtypes = [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                               C.POINTER(C.c_int)]
+_lib.wd_get_stencil.argtypes = [_vp, C.c_int, _dp, _vp]
+_lib.wd_apply.argtypes = [_vp, C.c_int, _dp, _dp, _vp]
+_lib.wd_smooth.argtypes = [_vp, C.c_int, _dp, _dp, C.c_int, _vp]
+_lib.wd_restrict.argtypes = [_vp, C.c_int, _dp, _dp, _vp]
+_lib.wd_prolong.argtypes = [_vp, C.c_int, _dp, _dp, _vp]
+_lib.wd_coarse_solve.argtypes = [_vp, _dp, _dp, _vp]
+_lib.wd_residual_norm.argtypes = [_vp, _dp, _dp, C.POINTER(C.c_double),
+                                  C.POINTER(C.c_double), _vp]
+
+_lib.wd_profile_read.argtypes = [_vp, C.POINTER(C.c_double), C.c_int]
+_lib.wd_profile_reset.argtypes = [_vp]
+_lib.wd_launch_count.restype = C.c_longlong
+
+# every symbol include/wd.h declares
+ABI_SYMBOLS = ["wd_default_options", "wd_assemble", "wd_rhs", "wd_vcycle", "wd_solve",
+               "wd_recover_wind", "wd_destroy", "wd_last_error", "wd_device_bytes",
+               "wd_num_levels", "wd_level_dims", "wd_level_plan", "wd_get_stencil",
+               "wd_apply", "wd_smooth", "wd_restrict", "wd_prolong", "wd_coarse_solve",
+               "wd_residual_norm", "wd_profile_read", "wd_profile_reset", "wd_launch_count"]
+
+
+class WDError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRNAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def last_error() -> str:
+    return _lib.wd_last_error().decode()
+
+
+def _check(rc, ok=(WD_OK,)):
+    if rc not in ok:
+        raise WDError(rc, last_error())
+    return rc
+
+
+def _ptr(t: torch.Tensor):
+    assert t.dtype == torch.float64, t.dtype
+    assert t.is_contiguous()
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(t: torch.Tensor):
+    if t.is_cuda:
+        return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+    return C.c_void_p(0)
+
+
+def default_options(**kw) -> wd_options:
+    o = wd_options()
+    _lib.wd_default_options(C.byref(o))
+    for k, v in kw.items():
+        if k == "coarsen_rule" and isinstance(v, str):
+            v = RULES[v]
+        setattr(o, k, v)
+    return o
+
+
+class Context:
+    """Owns a ``wd_ctx*`` (hierarchy and workspaces on the device)."""
+
+    def __init__(self, handle, dims, device):
+        self.h = handle
+        self.dims = dims        # (n1, n2, n3)
+        self.device = device
+
+    def __del__(self):
+        self.close()
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.wd_destroy(self.h)
+            self.h = None
+
+    @property
+    def node_shape(self):
+        n1, n2, n3 = self.dims
+        return (n3, n2, n1)
+
+    @property
+    def elem_shape(self):
+        n1, n2, n3 = self.dims
+        return (3, n3 - 1, n2 - 1, n1 - 1)
+
+    def device_bytes(self):
+        return int(_lib.wd_device_bytes(self.h))
+
+    def num_levels(self):
+        return int(_lib.wd_num_levels(self.h))
+
+    def level_dims(self, l):
+        d = (C.c_int * 3)()
+        _check(_lib.wd_level_dims(self.h, l, d))
+        return tuple(d)
+
+    def level_shape(self, l):
+        n1, n2, n3 = self.level_dims(l)
+        return (n3, n2, n1)
+
+    def level_plan(self, l):
+        hz = C.c_int()
+        kept = (C.c_int * 600)()
+        nk = C.c_int()
+        _check(_lib.wd_level_plan(self.h, l, C.byref(hz), kept, C.byref(nk)))
+        return dict(horizontal=bool(hz.value), kept=list(kept[:nk.value]))
+
+
+def wd_profile_read(ctx: Context):
+    out = (C.c_double * 6)()
+    _lib.wd_profile_read(ctx.h, out, 6)
+    keys = ("gs0_ms", "gs0_sweeps", "vcycle_ms", "vcycles", "resid_ms", "resids")
+    return dict(zip(keys, list(out)))
+
+
+def wd_profile_reset(ctx: Context):
+    _lib.wd_profile_reset(ctx.h)
+
+
+def wd_launch_count() -> int:
+    return int(_lib.wd_launch_count())
+
+
+# ------------------------------------------------------------------ ABI calls
+def wd_assemble(X, Y, Z, a, opt: wd_options | None = None) -> Context:
+    n3, n2, n1 = X.shape
+    h = C.c_void_p()
+    o = opt if opt is not None else default_options()
+    _check(_lib.wd_assemble(_ptr(X), _ptr(Y), _ptr(Z), n1, n2, n3, float(a[0]), float(a[1]),
+                            float(a[2]), C.byref(o), _stream(X), C.byref(h)))
+    return Context(h, (n1, n2, n3), X.device)
+
+
+def wd_rhs(ctx: Context, u0, f=None):
+    if f is None:
+        f = torch.empty(ctx.node_shape, dtype=torch.float64, device=u0.device)
+    _check(_lib.wd_rhs(ctx.h, _ptr(u0), _ptr(f), _stream(u0)))
+    return f
+
+
+def wd_vcycle(ctx: Context, lam, f, want_residual=True):
+    rel = C.c_double(0)
+    _check(_lib.wd_vcycle(ctx.h, _ptr(lam), _ptr(f), C.byref(rel) if want_residual else None,
+                          _stream(lam)))
+    return rel.value if want_residual else None
+
+
+def wd_solve(ctx: Context, f, lam0=None, rel_tol=1e-8, lam=None, raise_on_noconv=True):
+    if lam is None:
+        lam = torch.empty(ctx.node_shape, dtype=torch.float64, device=f.device)
+    rep = wd_report()
+    rc = _lib.wd_solve(ctx.h, _ptr(f), None if lam0 is None else _ptr(lam0), float(rel_tol),
+                       _ptr(lam), C.byref(rep), _stream(f))
+    ok = (WD_OK,) if raise_on_noconv else (WD_OK, WD_E_NOCONV, WD_E_DIVERGED, WD_E_NONFINITE)
+    _check(rc, ok)
+    return lam, rep.to_dict()
+
+
+def wd_recover_wind(ctx: Context, lam, u0, u=None):
+    if u is None:
+        u = torch.empty_like(u0)
+    _check(_lib.wd_recover_wind(ctx.h, _ptr(lam), _ptr(u0), _ptr(u), _stream(u0)))
+    return u
+
+
+# ------------------------------------------------------------------ inspection
+def wd_get_stencil(ctx: Context, level=0, device=None):
+    n3, n2, n1 = ctx.level_shape(level)
+    K = torch.empty((n3, n2, n1, 27), dtype=torch.float64, device=device or ctx.device)
+    _check(_lib.wd_get_stencil(ctx.h, level, _ptr(K), _stream(K)))
+    return K
+
+
+def wd_apply(ctx: Context, level, x, y=None):
+    y = torch.empty_like(x) if y is None else y
+    _check(_lib.wd_apply(ctx.h, level, _ptr(x), _ptr(y), _stream(x)))
+    return y
+
+
+def wd_smooth(ctx: Context, level, x, f, sweeps=1):
+    _check(_lib.wd_smooth(ctx.h, level, _ptr(x), _ptr(f), int(sweeps), _stream(x)))
+    return x
+
+
+def wd_restrict(ctx: Context, level, r, fc=None):
+    if fc is None:
+        fc = torch.empty(ctx.level_shape(level + 1), dtype=torch.float64, device=r.device)
+    _check(_lib.wd_restrict(ctx.h, level, _ptr(r), _ptr(fc), _stream(r)))
+    return fc
+
+
+def wd_prolong(ctx: Context, level, xc, x):
+    _check(_lib.wd_prolong(ctx.h, level, _ptr(xc), _ptr(x), _stream(x)))
+    return x
+
+
+def wd_coarse_solve(ctx: Context, f, x=None):
+    x = torch.empty_like(f) if x is None else x
+    _check(_lib.wd_coarse_solve(ctx.h, _ptr(f), _ptr(x), _stream(f)))
+    return x
+
+
+def wd_residual_norm(ctx: Context, x, f):
+    a = C.c_double()
+    r = C.c_double()
+    _check(_lib.wd_residual_norm(ctx.h, _ptr(x), _ptr(f), C.byref(a), C.byref(r), _stream(x)))
+    return a.value, r.value
+
+
+def downscale(X, Y, Z, u0, a, rel_tol=1e-8, lam0=None, opt=None):
+    """End to end through the public ABI: assemble, RHS, solve, recover.
+    Inputs may be host or device tensors (host buffers are staged inside the
+    library calls).  Returns (u, lam, report)."""
+    ctx = wd_assemble(X, Y, Z, a, opt)
+    try:
+        f = wd_rhs(ctx, u0, torch.empty(ctx.node_shape, dtype=torch.float64, device=u0.device))
+        lam, rep = wd_solve(ctx, f, lam0, rel_tol)
+        u = wd_recover_wind(ctx, lam, u0)
+    finally:
+        ctx.close()
+    return u, lam, rep

@@ -1,0 +1,359 @@
+// k_fe.cu -- finite-element kernels for sm_100a, fp64 (Sec. 2).
+//
+//   assemble_kernel : element stiffness by 2x2x2 Gauss quadrature
+//                     gathered into the 14-coefficient symmetric nodal stencil,
+//                     fused with mesh validation (detJ > 0, Z increasing).
+//   rhs_kernel      : one-point RHS f = -int grad mu . u0.
+//   recover_kernel  : u = u0 + A^{-1} grad lambda at element centres
+//                     (Eq. (3)).
+// The RHS and recovery kernels share one centre-derivative routine
+// (centre_jacobian), as P:112-114 prescribes.
+//
+// Tiling: a CTA owns a (TX-1) x (TY-1) tile of node columns and computes the
+// TX x TY element columns around it (1-element halo recomputed), streaming
+// upward in k.  Element results go to shared memory; each node thread gathers
+// its couplings from the 4 element columns in a fixed order (deterministic,
+// no atomics).  Partial sums of the node level k+1 (contributions of the
+// element level k) stay in registers until element level k+1 completes them.
+#include "wd_internal.cuh"
+
+namespace wd {
+
+namespace {
+
+constexpr int TX = 32, TY = 8, NTH = TX * TY;   // element columns per CTA
+constexpr double GP = 0.57735026918962576451;  // 1/sqrt(3)
+
+__host__ __device__ constexpr double sgn(int a, int d) { return ((a >> d) & 1) ? 1.0 : -1.0; }
+
+// dN_a/dxi_d at reference point xi (compile-time constant when xi is)
+__host__ __device__ constexpr double dN(int a, int d, double x0, double x1, double x2) {
+    return d == 0 ? 0.5 * sgn(a, 0) * 0.5 * (1.0 + sgn(a, 1) * x1) * 0.5 * (1.0 + sgn(a, 2) * x2)
+         : d == 1 ? 0.5 * sgn(a, 1) * 0.5 * (1.0 + sgn(a, 0) * x0) * 0.5 * (1.0 + sgn(a, 2) * x2)
+                  : 0.5 * sgn(a, 2) * 0.5 * (1.0 + sgn(a, 0) * x0) * 0.5 * (1.0 + sgn(a, 1) * x1);
+}
+
+__host__ __device__ constexpr int ut(int a, int b) { return a * (15 - a) / 2 + b; }  // a <= b
+
+// J[m][d] = sum_a x[a][m] dN_a/dxi_d ; returns det and Ji = J^{-1} (Ji[d][m])
+__device__ __forceinline__ double jac_inv(const double (&x)[8][3], double x0, double x1,
+                                          double x2, double (&Ji)[3][3]) {
+    double J[3][3];
+#pragma unroll
+    for (int m = 0; m < 3; m++)
+#pragma unroll
+        for (int d = 0; d < 3; d++) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < 8; a++) s = fma(x[a][m], dN(a, d, x0, x1, x2), s);
+            J[m][d] = s;
+        }
+    double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    double id = 1.0 / det;
+    Ji[0][0] = c00 * id;
+    Ji[1][0] = c01 * id;
+    Ji[2][0] = c02 * id;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+    return det;
+}
+
+// Centre geometry shared by the RHS and the recovery.
+__device__ __forceinline__ double centre_jacobian(const double (&x)[8][3], double (&Ji)[3][3]) {
+    return jac_inv(x, 0.0, 0.0, 0.0, Ji);
+}
+
+// Upper triangle of the element stiffness,
+//   Ke_ab = sum_g detJ_g grad N_a . diag(c) grad N_b
+//         = sum_g sum_{d,e} dN_a/dxi_d (detJ_g Ji c Ji^T)_{de} dN_b/dxi_e,
+// accumulated Gauss point by Gauss point (weights 1).  Returns the first
+// failing Gauss point + 1, or 0.
+__device__ __forceinline__ int element_stiffness(const double (&x)[8][3], double c0, double c1,
+                                                 double c2, double (&K)[36]) {
+    int badg = 0;
+#pragma unroll
+    for (int t = 0; t < 36; t++) K[t] = 0.0;
+#pragma unroll
+    for (int g = 0; g < 8; g++) {
+        const double x0 = (g & 1) ? GP : -GP;
+        const double x1 = (g & 2) ? GP : -GP;
+        const double x2 = (g & 4) ? GP : -GP;
+        double Ji[3][3];
+        double det = jac_inv(x, x0, x1, x2, Ji);
+        if (!(det > 0.0) && badg == 0) badg = g + 1;
+        // M = det * Ji diag(c) Ji^T  (symmetric 3x3)
+        double M[3][3];
+#pragma unroll
+        for (int d = 0; d < 3; d++)
+#pragma unroll
+            for (int e = d; e < 3; e++) {
+                double s = c0 * Ji[d][0] * Ji[e][0];
+                s = fma(c1 * Ji[d][1], Ji[e][1], s);
+                s = fma(c2 * Ji[d][2], Ji[e][2], s);
+                M[d][e] = det * s;
+                M[e][d] = M[d][e];
+            }
+#pragma unroll
+        for (int a = 0; a < 8; a++)
+#pragma unroll
+            for (int b = a; b < 8; b++) {
+                double s = K[ut(a, b)];
+#pragma unroll
+                for (int d = 0; d < 3; d++)
+#pragma unroll
+                    for (int e = 0; e < 3; e++)
+                        s = fma(dN(a, d, x0, x1, x2) * dN(b, e, x0, x1, x2), M[d][e], s);
+                K[ut(a, b)] = s;
+            }
+    }
+    return badg;
+}
+
+__device__ __forceinline__ void load_plane(const double* __restrict__ X,
+                                           const double* __restrict__ Y,
+                                           const double* __restrict__ Z, int n1, int n2, int i,
+                                           int j, int k, double (&x)[8][3], int top) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        i64 p = ((i64)k * n2 + (j + (q >> 1))) * n1 + (i + (q & 1));
+        x[q + 4 * top][0] = __ldg(X + p);
+        x[q + 4 * top][1] = __ldg(Y + p);
+        x[q + 4 * top][2] = __ldg(Z + p);
+    }
+}
+
+// node-side gather of the element-level couplings: node is local index
+// a = (1-ex) + 2(1-ey) + 4 dc in the element column (ex, ey) of its 2x2.
+template <int DC>
+__device__ __forceinline__ void gather_couplings(const double* ke, int t, double (&acc)[14]) {
+#pragma unroll
+    for (int ey = 0; ey < 2; ey++)
+#pragma unroll
+        for (int ex = 0; ex < 2; ex++) {
+            const int te = t + ex + ey * TX;
+            const int a = (1 - ex) + 2 * (1 - ey) + 4 * DC;
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                const int s = slot_of((b & 1) - (a & 1), ((b >> 1) & 1) - ((a >> 1) & 1),
+                                      ((b >> 2) & 1) - DC);
+                if (s >= 0) {
+                    const int u = a <= b ? ut(a, b) : ut(b, a);
+                    acc[s] += ke[u * NTH + te];
+                }
+            }
+        }
+}
+
+__global__ void __launch_bounds__(NTH, 1)
+assemble_kernel(const double* __restrict__ X, const double* __restrict__ Y,
+                const double* __restrict__ Z, int n1, int n2, int n3, double c0, double c1,
+                double c2, LevDev L, double* __restrict__ coef, unsigned long long* bad) {
+    extern __shared__ double ke[];   // [36][NTH]
+    const int t = threadIdx.x;
+    const int tx = t % TX, ty = t / TX;
+    const int i0 = blockIdx.x * (TX - 1), j0 = blockIdx.y * (TY - 1);
+    const int ei = i0 - 1 + tx, ej = j0 - 1 + ty;
+    const bool ev = ei >= 0 && ei < n1 - 1 && ej >= 0 && ej < n2 - 1;
+    const int ni = i0 + tx, nj = j0 + ty;
+    const bool nv = tx < TX - 1 && ty < TY - 1 && ni < n1 && nj < n2;
+    const int nx = n1 - 1, ny = n2 - 1;
+
+    double x[8][3];
+    if (ev) load_plane(X, Y, Z, n1, n2, ei, ej, 0, x, 0);
+    double acc[14];
+#pragma unroll
+    for (int s = 0; s < 14; s++) acc[s] = 0.0;
+    for (int ek = 0; ek < n3 - 1; ek++) {
+        double K[36];
+        if (ev) {
+            load_plane(X, Y, Z, n1, n2, ei, ej, ek + 1, x, 1);
+            int badg = element_stiffness(x, c0, c1, c2, K);
+            int zbad = 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++) zbad |= !(x[q + 4][2] > x[q][2]);
+            if (zbad || badg) {
+                unsigned long long e = ((unsigned long long)ek * ny + ej) * nx + ei;
+                atomicMin(bad, e * 16ull + (zbad ? 0ull : (unsigned long long)badg));
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                x[q][0] = x[q + 4][0];
+                x[q][1] = x[q + 4][1];
+                x[q][2] = x[q + 4][2];
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 36; u++) K[u] = 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 36; u++) ke[u * NTH + t] = K[u];
+        __syncthreads();
+        if (nv) {
+            gather_couplings<0>(ke, t, acc);   // node level ek as a bottom node
+            const i64 o = loff(L, ni, nj, ek);
+#pragma unroll
+            for (int s = 0; s < 14; s++) coef[s * L.NT + o] = acc[s];
+#pragma unroll
+            for (int s = 0; s < 14; s++) acc[s] = 0.0;
+            gather_couplings<1>(ke, t, acc);   // node level ek+1 as a top node
+        }
+        __syncthreads();
+    }
+    if (nv) {
+        const i64 o = loff(L, ni, nj, n3 - 1);
+#pragma unroll
+        for (int s = 0; s < 14; s++) coef[s * L.NT + o] = acc[s];
+    }
+}
+
+// ------------------------------------------------------------------ RHS
+// f_p = sum_{e ni p} fe_a(p),  fe_a = -8 detJ(0) gradN_a(0).u0_e
+//     = -detJ(0) sum_d s_ad (Ji(0) u0_e)_d          (dN_a/dxi_d(0) = s_ad/8)
+__global__ void __launch_bounds__(NTH)
+rhs_kernel(const double* __restrict__ X, const double* __restrict__ Y,
+           const double* __restrict__ Z, int n1, int n2, int n3,
+           const double* __restrict__ u0, double* __restrict__ f) {
+    __shared__ double fe[8][NTH];
+    const int t = threadIdx.x;
+    const int tx = t % TX, ty = t / TX;
+    const int i0 = blockIdx.x * (TX - 1), j0 = blockIdx.y * (TY - 1);
+    const int ei = i0 - 1 + tx, ej = j0 - 1 + ty;
+    const int nx = n1 - 1, ny = n2 - 1, nz = n3 - 1;
+    const bool ev = ei >= 0 && ei < nx && ej >= 0 && ej < ny;
+    const int ni = i0 + tx, nj = j0 + ty;
+    const bool nv = tx < TX - 1 && ty < TY - 1 && ni < n1 && nj < n2;
+    const bool ndir = ni == 0 || ni == n1 - 1 || nj == 0 || nj == n2 - 1;
+    const i64 E = (i64)nx * ny * nz;
+    double x[8][3];
+    if (ev) load_plane(X, Y, Z, n1, n2, ei, ej, 0, x, 0);
+    double top = 0.0;   // contributions to node level ek from element level ek-1
+    for (int ek = 0; ek < nz; ek++) {
+        double v[8];
+        if (ev) {
+            load_plane(X, Y, Z, n1, n2, ei, ej, ek + 1, x, 1);
+            const i64 e = ((i64)ek * ny + ej) * nx + ei;
+            const double u = __ldg(u0 + e), w1 = __ldg(u0 + E + e), w2 = __ldg(u0 + 2 * E + e);
+            double Ji[3][3];
+            const double det = centre_jacobian(x, Ji);
+            double g[3];
+#pragma unroll
+            for (int d = 0; d < 3; d++) g[d] = Ji[d][0] * u + Ji[d][1] * w1 + Ji[d][2] * w2;
+#pragma unroll
+            for (int a = 0; a < 8; a++)
+                v[a] = -det * (sgn(a, 0) * g[0] + sgn(a, 1) * g[1] + sgn(a, 2) * g[2]);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                x[q][0] = x[q + 4][0];
+                x[q][1] = x[q + 4][1];
+                x[q][2] = x[q + 4][2];
+            }
+        } else {
+#pragma unroll
+            for (int a = 0; a < 8; a++) v[a] = 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < 8; a++) fe[a][t] = v[a];
+        __syncthreads();
+        if (nv) {
+            double s = top, s2 = 0.0;
+#pragma unroll
+            for (int ey = 0; ey < 2; ey++)
+#pragma unroll
+                for (int ex = 0; ex < 2; ex++) {
+                    const int te = t + ex + ey * TX;
+                    const int a = (1 - ex) + 2 * (1 - ey);
+                    s += fe[a][te];
+                    s2 += fe[a + 4][te];
+                }
+            f[((i64)ek * n2 + nj) * n1 + ni] = ndir ? 0.0 : s;
+            top = s2;
+        }
+        __syncthreads();
+    }
+    if (nv) f[((i64)nz * n2 + nj) * n1 + ni] = 0.0;   // top plane is Dirichlet
+}
+
+// ------------------------------------------------------------------ recovery
+// u_e = u0_e + c .* (Ji(0)^T g),  g_d = sum_a lambda_a s_ad / 8
+__global__ void __launch_bounds__(256)
+recover_kernel(const double* __restrict__ X, const double* __restrict__ Y,
+               const double* __restrict__ Z, int n1, int n2, int n3, double c0, double c1,
+               double c2, const double* __restrict__ lam, const double* __restrict__ u0,
+               double* __restrict__ u) {
+    const int ei = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ej = blockIdx.y;
+    const int nx = n1 - 1, ny = n2 - 1, nz = n3 - 1;
+    if (ei >= nx) return;
+    const i64 E = (i64)nx * ny * nz;
+    double x[8][3], l[8];
+    load_plane(X, Y, Z, n1, n2, ei, ej, 0, x, 0);
+#pragma unroll
+    for (int q = 0; q < 4; q++) l[q] = __ldg(lam + (i64)(ej + (q >> 1)) * n1 + ei + (q & 1));
+    for (int ek = 0; ek < nz; ek++) {
+        load_plane(X, Y, Z, n1, n2, ei, ej, ek + 1, x, 1);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            l[q + 4] = __ldg(lam + ((i64)(ek + 1) * n2 + ej + (q >> 1)) * n1 + ei + (q & 1));
+        double Ji[3][3];
+        centre_jacobian(x, Ji);
+        double g[3];
+#pragma unroll
+        for (int d = 0; d < 3; d++) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < 8; a++) s = fma(l[a], sgn(a, d), s);
+            g[d] = 0.125 * s;
+        }
+        const i64 e = ((i64)ek * ny + ej) * nx + ei;
+        const double gx = Ji[0][0] * g[0] + Ji[1][0] * g[1] + Ji[2][0] * g[2];
+        const double gy = Ji[0][1] * g[0] + Ji[1][1] * g[1] + Ji[2][1] * g[2];
+        const double gz = Ji[0][2] * g[0] + Ji[1][2] * g[1] + Ji[2][2] * g[2];
+        const double a0 = __ldg(u0 + e), a1 = __ldg(u0 + E + e), a2 = __ldg(u0 + 2 * E + e);
+        u[e] = fma(c0, gx, a0);
+        u[E + e] = fma(c1, gy, a1);
+        u[2 * E + e] = fma(c2, gz, a2);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            x[q][0] = x[q + 4][0];
+            x[q][1] = x[q + 4][1];
+            x[q][2] = x[q + 4][2];
+            l[q] = l[q + 4];
+        }
+    }
+}
+
+}  // namespace
+
+void launch_assemble(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
+                     const double c[3], const LevDev& L, double* coef, unsigned long long* bad,
+                     cudaStream_t st) {
+    const size_t smem = sizeof(double) * 36 * NTH;
+    cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((n1 + TX - 2) / (TX - 1), (n2 + TY - 2) / (TY - 1));
+    g_launches += 1;
+    assemble_kernel<<<grid, NTH, smem, st>>>(X, Y, Z, n1, n2, n3, c[0], c[1], c[2], L, coef, bad);
+}
+
+void launch_rhs(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
+                const double* u0, double* f, cudaStream_t st) {
+    dim3 grid((n1 + TX - 2) / (TX - 1), (n2 + TY - 2) / (TY - 1));
+    g_launches += 1;
+    rhs_kernel<<<grid, NTH, 0, st>>>(X, Y, Z, n1, n2, n3, u0, f);
+}
+
+void launch_recover(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
+                    const double c[3], const double* lam, const double* u0, double* u,
+                    cudaStream_t st) {
+    dim3 grid((n1 - 1 + 127) / 128, n2 - 1);
+    g_launches += 1;
+    recover_kernel<<<grid, 128, 0, st>>>(X, Y, Z, n1, n2, n3, c[0], c[1], c[2], lam, u0, u);
+}
+
+}  // namespace wd

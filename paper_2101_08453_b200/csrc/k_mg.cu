@@ -1,0 +1,473 @@
+// k_mg.cu -- multigrid kernels on the 14-coefficient stencil (Sec. 3).
+//
+//   gs_phase_kernel  : one colour phase of the smoother, "vertical sweeps of
+//                      Gauss-Seidel from the bottom up to the top, with
+//                      red-black ordering horizontally into 4 groups"
+//                      (P:174-176).  One thread per column of the colour,
+//                      sequential in k, lambda of the 9 columns kept in a
+//                      3-level register window.
+//   apply_kernel     : y = K x  or  r = f - K x with deterministic block
+//                      partial sums of r^2 (Eq. (7) residual, convergence test).
+//   restrict_kernel  : f_c = P^T r  (Eq. (7), gather form, fixed order).
+//   prolong_kernel   : x += P x_c   (Eq. (7)).
+//   galerkin_kernel  : K_c = P^T K P (Eq. (7)) on the 14 forward slots.
+// P is the index-space trilinear interpolation of P:176-181 (weights 1 and
+// 1/2 per direction, tensor product), described by per-direction maps.
+#include "wd_internal.cuh"
+
+namespace wd {
+
+namespace {
+
+constexpr int GS_BLK = 128;
+constexpr int AP_BLK = 128;
+
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+
+// column offsets (same level) of the 9 columns (ox,oy) around (i,j), i of parity ci:
+// c = (ox+1) + 3(oy+1)
+__device__ __forceinline__ void column_offsets(const LevDev& L, int ci, i64 (&co)[9]) {
+    const i64 xm = ci ? -(i64)L.H : (i64)L.H - 1;   // i-1 lives in the other half
+    const i64 xp = ci ? 1 - (i64)L.H : (i64)L.H;    // i+1
+#pragma unroll
+    for (int oy = -1; oy <= 1; oy++) {
+        co[0 + 3 * (oy + 1)] = (i64)oy * L.P + xm;
+        co[1 + 3 * (oy + 1)] = (i64)oy * L.P;
+        co[2 + 3 * (oy + 1)] = (i64)oy * L.P + xp;
+    }
+}
+
+__device__ __forceinline__ int cidx(int ox, int oy) { return (ox + 1) + 3 * (oy + 1); }
+
+// sum_{q != p} K_pq x_q for node p at level k of column `o` (offset of level 0),
+// with x of the 9 columns at levels k-1, k, k+1 in xm, x0, xp.
+__device__ __forceinline__ double offdiag(const LevDev& L, const double* __restrict__ K,
+                                          i64 base, const i64 (&co)[9], const double (&xm)[9],
+                                          const double (&x0)[9], const double (&xp)[9],
+                                          bool has_below) {
+    const i64 NT = L.NT;
+    double s = 0.0;
+    // forward couplings K(p, p + d_s) stored at p
+#pragma unroll
+    for (int sl = 1; sl < 14; sl++) {
+        const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+        const double kv = ldg(K + sl * NT + base);
+        s = fma(kv, dz ? xp[cidx(dx, dy)] : x0[cidx(dx, dy)], s);
+    }
+    // backward couplings K(p, p - d_s) stored at p - d_s
+#pragma unroll
+    for (int sl = 1; sl < 14; sl++) {
+        const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+        if (dz) {
+            if (has_below) {
+                const double kv = ldg(K + sl * NT + base - L.plane + co[cidx(-dx, -dy)]);
+                s = fma(kv, xm[cidx(-dx, -dy)], s);
+            }
+        } else {
+            const double kv = ldg(K + sl * NT + base + co[cidx(-dx, -dy)]);
+            s = fma(kv, x0[cidx(-dx, -dy)], s);
+        }
+    }
+    return s;
+}
+
+__global__ void __launch_bounds__(GS_BLK)
+gs_phase_kernel(LevDev L, const double* __restrict__ K, double* lam,
+                const double* __restrict__ f, int ci, int cj) {
+    const int a = blockIdx.x * GS_BLK + threadIdx.x;
+    const int i = 2 * a + ci;
+    const int j = 2 * blockIdx.y + cj;
+    if (i < 1 || i > L.n1 - 2 || j < 1 || j > L.n2 - 2) return;
+    i64 co[9];
+    column_offsets(L, ci, co);
+    const i64 own = loff(L, i, j, 0);
+    double xm[9], x0[9], xp[9];
+#pragma unroll
+    for (int c = 0; c < 9; c++) {
+        xm[c] = 0.0;
+        x0[c] = c == 4 ? lam[own] : ldg(lam + own + co[c]);
+        xp[c] = c == 4 ? lam[own + L.plane] : ldg(lam + own + L.plane + co[c]);
+    }
+    const int kt = L.n3 - 2;   // top free level
+    for (int k = 0; k <= kt; k++) {
+        const i64 base = own + (i64)k * L.plane;
+        const double s = offdiag(L, K, base, co, xm, x0, xp, k > 0);
+        const double v = (ldg(f + base) - s) / ldg(K + base);
+        lam[base] = v;
+        x0[4] = v;
+#pragma unroll
+        for (int c = 0; c < 9; c++) {
+            xm[c] = x0[c];
+            x0[c] = xp[c];
+        }
+        if (k + 2 <= L.n3 - 1) {
+            const i64 nb = base + 2 * L.plane;
+#pragma unroll
+            for (int c = 0; c < 9; c++) xp[c] = c == 4 ? lam[nb] : ldg(lam + nb + co[c]);
+        }
+    }
+}
+
+// deterministic block reduction (warp shuffle tree + fixed-order smem)
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double ws[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) ws[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        for (int t = 0; t < nw; t++) r += ws[t];
+    }
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(AP_BLK)
+apply_kernel(LevDev L, const double* __restrict__ K, const double* __restrict__ x,
+             const double* __restrict__ f, double* __restrict__ y, double* __restrict__ partial) {
+    const int a = blockIdx.x * AP_BLK + threadIdx.x;
+    const int j = blockIdx.y;
+    const int ci = blockIdx.z;
+    const int i = 2 * a + ci;
+    double acc = 0.0;
+    if (i >= 1 && i <= L.n1 - 2 && j >= 1 && j <= L.n2 - 2) {
+        i64 co[9];
+        column_offsets(L, ci, co);
+        const i64 own = loff(L, i, j, 0);
+        double xm[9], x0[9], xp[9];
+#pragma unroll
+        for (int c = 0; c < 9; c++) {
+            xm[c] = 0.0;
+            x0[c] = ldg(x + own + co[c]);
+            xp[c] = ldg(x + own + L.plane + co[c]);
+        }
+        for (int k = 0; k <= L.n3 - 2; k++) {
+            const i64 base = own + (i64)k * L.plane;
+            double s = offdiag(L, K, base, co, xm, x0, xp, k > 0);
+            s = fma(ldg(K + base), x0[4], s);
+            const double v = f ? ldg(f + base) - s : s;
+            y[base] = v;
+            acc = fma(v, v, acc);
+#pragma unroll
+            for (int c = 0; c < 9; c++) {
+                xm[c] = x0[c];
+                x0[c] = xp[c];
+            }
+            if (k + 2 <= L.n3 - 1) {
+                const i64 nb = base + 2 * L.plane;
+#pragma unroll
+                for (int c = 0; c < 9; c++) xp[c] = ldg(x + nb + co[c]);
+            }
+        }
+    }
+    if (partial) {
+        const double s = block_sum(acc);
+        if (threadIdx.x == 0)
+            partial[((i64)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
+    }
+}
+
+__global__ void __launch_bounds__(1024) reduce_kernel(const double* __restrict__ p, int n,
+                                                      double* out) {
+    double v = 0.0;
+    for (int t = threadIdx.x; t < n; t += 1024) v += p[t];
+    v = block_sum(v);
+    if (threadIdx.x == 0) *out = v;
+}
+
+__global__ void __launch_bounds__(256) norm2_partial_kernel(const double* __restrict__ v, i64 n,
+                                                             double* partial) {
+    double acc = 0.0;
+    const i64 stride = (i64)gridDim.x * 256;
+    for (i64 t = (i64)blockIdx.x * 256 + threadIdx.x; t < n; t += stride) {
+        const double a = v[t];
+        acc = fma(a, a, acc);
+    }
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+
+// natural [k][j][i] <-> internal i-split layout
+__global__ void nat2int_kernel(LevDev L, const double* __restrict__ src, double* __restrict__ dst,
+                               int zero_dir) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, k = blockIdx.z;
+    if (i >= L.n1) return;
+    double v = src[((i64)k * L.n2 + j) * L.n1 + i];
+    if (zero_dir && (i == 0 || i == L.n1 - 1 || j == 0 || j == L.n2 - 1 || k == L.n3 - 1))
+        v = 0.0;
+    dst[loff(L, i, j, k)] = v;
+}
+
+__global__ void int2nat_kernel(LevDev L, const double* __restrict__ src, double* __restrict__ dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, k = blockIdx.z;
+    if (i >= L.n1) return;
+    dst[((i64)k * L.n2 + j) * L.n1 + i] = src[loff(L, i, j, k)];
+}
+
+__global__ void zero_dirichlet_kernel(LevDev L, double* v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, k = blockIdx.z;
+    if (i >= L.n1) return;
+    if (i == 0 || i == L.n1 - 1 || j == 0 || j == L.n2 - 1 || k == L.n3 - 1) v[loff(L, i, j, k)] = 0.0;
+}
+
+// 1-D support of coarse index c along one direction: fine indices and weights
+__device__ __forceinline__ int support1d(const int* __restrict__ pos, const int* __restrict__ co,
+                                         int n, int c, int (&t)[3], double (&w)[3]) {
+    const int p = pos[c];
+    int m = 0;
+    if (p - 1 >= 0 && !co[p - 1]) { t[m] = p - 1; w[m] = 0.5; m++; }
+    t[m] = p; w[m] = 1.0; m++;
+    if (p + 1 < n && !co[p + 1]) { t[m] = p + 1; w[m] = 0.5; m++; }
+    return m;
+}
+
+__global__ void __launch_bounds__(128)
+restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
+                double* __restrict__ fc) {
+    const int I = blockIdx.x * 128 + threadIdx.x;
+    const int J = blockIdx.y;
+    if (I < 1 || I > C.n1 - 2 || J < 1 || J > C.n2 - 2) return;
+    int tx[3], ty[3];
+    double wx[3], wy[3];
+    const int mx = support1d(M.pos[0], M.co[0], F.n1, I, tx, wx);
+    const int my = support1d(M.pos[1], M.co[1], F.n2, J, ty, wy);
+    for (int Kc = 0; Kc <= C.n3 - 2; Kc++) {
+        int tz[3];
+        double wz[3];
+        const int mz = support1d(M.pos[2], M.co[2], F.n3, Kc, tz, wz);
+        double s = 0.0;
+        for (int c = 0; c < mz; c++)
+            for (int b = 0; b < my; b++) {
+                double sr = 0.0;
+                for (int a = 0; a < mx; a++) sr = fma(wx[a], ldg(r + loff(F, tx[a], ty[b], tz[c])), sr);
+                s = fma(wz[c] * wy[b], sr, s);
+            }
+        fc[loff(C, I, J, Kc)] = s;
+    }
+}
+
+__global__ void __launch_bounds__(128)
+prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc, double* x) {
+    const int i = blockIdx.x * 128 + threadIdx.x;
+    const int j = blockIdx.y;
+    if (i < 1 || i > F.n1 - 2 || j < 1 || j > F.n2 - 2) return;
+    const int ix = M.lo[0][i], iy = M.lo[1][j];
+    const int nx = M.co[0][i] ? 1 : 2, ny = M.co[1][j] ? 1 : 2;
+    const double wx = nx == 1 ? 1.0 : 0.5, wy = ny == 1 ? 1.0 : 0.5;
+    for (int k = 0; k <= F.n3 - 2; k++) {
+        const int iz = M.lo[2][k];
+        const int nz = M.co[2][k] ? 1 : 2;
+        const double wz = nz == 1 ? 1.0 : 0.5;
+        double s = 0.0;
+        for (int c = 0; c < nz; c++)
+            for (int b = 0; b < ny; b++) {
+                double sr = 0.0;
+                for (int a = 0; a < nx; a++) sr += ldg(xc + loff(C, ix + a, iy + b, iz + c));
+                s = fma(wy * wz, wx * sr, s);
+            }
+        const i64 o = loff(F, i, j, k);
+        x[o] += s;
+    }
+}
+
+// K(p, p + d) from 14-slot storage (d in {-1,0,1}^3, both ends inside the grid)
+__device__ __forceinline__ double kget(const LevDev& L, const double* __restrict__ K, int i, int j,
+                                       int k, int dx, int dy, int dz) {
+    const int s = slot_of(dx, dy, dz);
+    if (s >= 0) return ldg(K + s * L.NT + loff(L, i, j, k));
+    return ldg(K + (-s) * L.NT + loff(L, i + dx, j + dy, k + dz));
+}
+
+__global__ void __launch_bounds__(128)
+galerkin_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ KF,
+                double* __restrict__ KC) {
+    const int I = blockIdx.x * 128 + threadIdx.x;
+    const int J = blockIdx.y, Kc = blockIdx.z;
+    if (I < 1 || I > C.n1 - 2 || J < 1 || J > C.n2 - 2 || Kc > C.n3 - 2) return;
+    int pt[3][3];
+    double pw[3][3];
+    int pm[3];
+    pm[0] = support1d(M.pos[0], M.co[0], F.n1, I, pt[0], pw[0]);
+    pm[1] = support1d(M.pos[1], M.co[1], F.n2, J, pt[1], pw[1]);
+    pm[2] = support1d(M.pos[2], M.co[2], F.n3, Kc, pt[2], pw[2]);
+    const int nd[3] = {F.n1, F.n2, F.n3};
+    const int Pc[3] = {I, J, Kc};
+    const i64 out = loff(C, I, J, Kc);
+    for (int sl = 0; sl < 14; sl++) {
+        const int d[3] = {slot_dx(sl), slot_dy(sl), slot_dz(sl)};
+        // per-direction pair lists (p_t, q_t - p_t, w_P w_Q) with |q_t - p_t| <= 1
+        int lt[3][9], ld[3][9];
+        double lw[3][9];
+        int ln[3];
+#pragma unroll
+        for (int e = 0; e < 3; e++) {
+            int qt[3];
+            double qw[3];
+            const int qm = support1d(M.pos[e], M.co[e], nd[e], Pc[e] + d[e], qt, qw);
+            int n = 0;
+            for (int u = 0; u < pm[e]; u++)
+                for (int v = 0; v < qm; v++) {
+                    const int dd = qt[v] - pt[e][u];
+                    if (dd >= -1 && dd <= 1) {
+                        lt[e][n] = pt[e][u];
+                        ld[e][n] = dd;
+                        lw[e][n] = pw[e][u] * qw[v];
+                        n++;
+                    }
+                }
+            ln[e] = n;
+        }
+        double s = 0.0;
+        for (int c = 0; c < ln[2]; c++)
+            for (int b = 0; b < ln[1]; b++) {
+                double sr = 0.0;
+                for (int a = 0; a < ln[0]; a++)
+                    sr = fma(lw[0][a], kget(F, KF, lt[0][a], lt[1][b], lt[2][c], ld[0][a], ld[1][b],
+                                            ld[2][c]), sr);
+                s = fma(lw[2][c] * lw[1][b], sr, s);
+            }
+        KC[sl * C.NT + out] = s;
+    }
+}
+
+__global__ void export27_kernel(LevDev L, const double* __restrict__ K, double* __restrict__ K27) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, k = blockIdx.z;
+    if (i >= L.n1) return;
+    const i64 p = ((i64)k * L.n2 + j) * L.n1 + i;
+    for (int o = 0; o < 27; o++) {
+        const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
+        const int ii = i + dx, jj = j + dy, kk = k + dz;
+        double v = 0.0;
+        if (ii >= 0 && ii < L.n1 && jj >= 0 && jj < L.n2 && kk >= 0 && kk < L.n3)
+            v = kget(L, K, i, j, k, dx, dy, dz);
+        K27[p * 27 + o] = v;
+    }
+}
+
+// argmin over the bottom plane (ties -> smallest index), two passes
+__global__ void argmin_kernel(const double* __restrict__ z, long long n,
+                              const long long* __restrict__ idx_in, double* pval,
+                              long long* pidx) {
+    __shared__ double sv[256];
+    __shared__ long long si[256];
+    double best = 1.0 / 0.0;
+    long long bi = 0x7fffffffffffffffll;
+    const long long stride = (long long)gridDim.x * 256;
+    for (long long t = (long long)blockIdx.x * 256 + threadIdx.x; t < n; t += stride) {
+        const double v = z[t];
+        const long long id = idx_in ? idx_in[t] : t;
+        if (v < best || (v == best && id < bi)) { best = v; bi = id; }
+    }
+    sv[threadIdx.x] = best;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            const double v = sv[threadIdx.x + o];
+            const long long id = si[threadIdx.x + o];
+            if (v < sv[threadIdx.x] || (v == sv[threadIdx.x] && id < si[threadIdx.x])) {
+                sv[threadIdx.x] = v;
+                si[threadIdx.x] = id;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        pval[blockIdx.x] = sv[0];
+        pidx[blockIdx.x] = si[0];
+    }
+}
+
+dim3 node_grid(const LevDev& L) { return dim3((L.n1 + 127) / 128, L.n2, L.n3); }
+
+}  // namespace
+
+void launch_nat2int(const LevDev& L, const double* src, double* dst, bool zero_dirichlet,
+                    cudaStream_t st) {
+    g_launches += 1;
+    nat2int_kernel<<<node_grid(L), 128, 0, st>>>(L, src, dst, zero_dirichlet ? 1 : 0);
+}
+
+void launch_int2nat(const LevDev& L, const double* src, double* dst, cudaStream_t st) {
+    g_launches += 1;
+    int2nat_kernel<<<node_grid(L), 128, 0, st>>>(L, src, dst);
+}
+
+void launch_zero_dirichlet(const LevDev& L, double* v, cudaStream_t st) {
+    g_launches += 1;
+    zero_dirichlet_kernel<<<node_grid(L), 128, 0, st>>>(L, v);
+}
+
+void launch_gs_sweep(const LevDev& L, const double* coef, double* lam, const double* f,
+                     cudaStream_t st) {
+    static const int colour[4][2] = {{0, 0}, {1, 0}, {0, 1}, {1, 1}};   // (i mod 2, j mod 2)
+    const int half = (L.n1 + 1) / 2;
+    dim3 grid((half + GS_BLK - 1) / GS_BLK, (L.n2 + 1) / 2);
+    g_launches += 4;
+    for (int c = 0; c < 4; c++)
+        gs_phase_kernel<<<grid, GS_BLK, 0, st>>>(L, coef, lam, f, colour[c][0], colour[c][1]);
+}
+
+int launch_apply(const LevDev& L, const double* coef, const double* x, const double* f, double* y,
+                 double* partial, cudaStream_t st) {
+    const int half = (L.n1 + 1) / 2;
+    dim3 grid((half + AP_BLK - 1) / AP_BLK, L.n2, 2);
+    g_launches += 1;
+    apply_kernel<<<grid, AP_BLK, 0, st>>>(L, coef, x, f, y, partial);
+    return (int)(grid.x * grid.y * grid.z);
+}
+
+void launch_reduce_sum(const double* partial, int n, double* out, cudaStream_t st) {
+    g_launches += 1;
+    reduce_kernel<<<1, 1024, 0, st>>>(partial, n, out);
+}
+
+void launch_norm2_partial(const LevDev& L, const double* v, double* partial, int* nblk,
+                          cudaStream_t st) {
+    const int nb = 1184;   // 8 x 148 SMs
+    g_launches += 1;
+    norm2_partial_kernel<<<nb, 256, 0, st>>>(v, L.NT, partial);
+    *nblk = nb;
+}
+
+void launch_restrict(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* r,
+                     double* fc, cudaStream_t st) {
+    dim3 grid((Cl.n1 + 127) / 128, Cl.n2);
+    g_launches += 1;
+    restrict_kernel<<<grid, 128, 0, st>>>(F, Cl, M, r, fc);
+}
+
+void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* xc,
+                    double* x, cudaStream_t st) {
+    dim3 grid((F.n1 + 127) / 128, F.n2);
+    g_launches += 1;
+    prolong_kernel<<<grid, 128, 0, st>>>(F, Cl, M, xc, x);
+}
+
+void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* coefF,
+                     double* coefC, unsigned int*, cudaStream_t st) {
+    dim3 grid((Cl.n1 + 127) / 128, Cl.n2, Cl.n3);
+    g_launches += 1;
+    galerkin_kernel<<<grid, 128, 0, st>>>(F, Cl, M, coefF, coefC);
+}
+
+void launch_export27(const LevDev& L, const double* coef, double* K27, cudaStream_t st) {
+    g_launches += 1;
+    export27_kernel<<<node_grid(L), 128, 0, st>>>(L, coef, K27);
+}
+
+void launch_argmin_bottom(const double* Z, int n, double* pval, long long* pidx, int nblk,
+                          cudaStream_t st) {
+    g_launches += 2;
+    argmin_kernel<<<nblk, 256, 0, st>>>(Z, n, nullptr, pval, pidx);
+    argmin_kernel<<<1, 256, 0, st>>>(pval, nblk, pidx, pval + nblk, pidx + nblk);
+}
+
+}  // namespace wd

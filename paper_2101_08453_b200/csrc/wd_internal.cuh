@@ -1,0 +1,107 @@
+// wd_internal.cuh -- shared definitions of the sm_100a kernels and the C ABI.
+//
+// Internal data layout in HBM ("i-split" layout):
+//   node (i,j,k) of a level lives at  off = k*plane + j*P + (i&1)*H + (i>>1)
+//   H = half-row pitch (ceil(n1/2) rounded up to 16 doubles = 128 B),
+//   P = 2H, plane = n2*P.  Within a row, even-i nodes come first and odd-i
+//   nodes second, so every colour phase of the 4-colour smoother
+//   ((i mod 2, j mod 2)) reads and writes stride-1 half rows.
+// Operator storage: 14 symmetric coefficients per node, SoA planes of NT
+// doubles each (coef[s*NT + off]):  s = 0 diagonal; s = 1..13 the "forward"
+// couplings K(p, p+d_s),  d_s in {(1,0,0), (-1,1,0), (0,1,0), (1,1,0),
+// (dx,dy,1) for dy, dx in -1..1}.  The backward coupling K(p, p-d_s) is read
+// from the node p-d_s, so the stored operator is symmetric by construction.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+namespace wd {
+
+// kernels launched by this library (defined in wd_api.cu); launchers add the
+// number of kernels they enqueue
+extern std::atomic<long long> g_launches;
+
+typedef long long i64;
+
+struct LevDev {
+    int n1, n2, n3;
+    int H, P;
+    i64 plane, NT;
+};
+
+__host__ __device__ __forceinline__ i64 loff(const LevDev& L, int i, int j, int k) {
+    return (i64)k * L.plane + (i64)j * L.P + (i64)((i & 1) * L.H + (i >> 1));
+}
+
+// forward offsets of the 14 slots (slot 0 = diagonal)
+__host__ __device__ __forceinline__ int slot_dx(int s) {
+    return s == 0 ? 0 : s == 1 ? 1 : s <= 4 ? (s - 3) : ((s - 5) % 3) - 1;
+}
+__host__ __device__ __forceinline__ int slot_dy(int s) {
+    return s <= 1 ? 0 : s <= 4 ? 1 : ((s - 5) / 3) - 1;
+}
+__host__ __device__ __forceinline__ int slot_dz(int s) { return s <= 4 ? 0 : 1; }
+
+// slot of offset (dx,dy,dz); returns +s for forward/zero offsets, -s for backward
+__host__ __device__ __forceinline__ int slot_of(int dx, int dy, int dz) {
+    if (dz == 1) return 5 + (dx + 1) + 3 * (dy + 1);
+    if (dz == -1) return -(5 + (-dx + 1) + 3 * (-dy + 1));
+    if (dy == 1) return 3 + dx;
+    if (dy == -1) return -(3 - dx);
+    if (dx == 1) return 1;
+    if (dx == -1) return -1;
+    return 0;
+}
+
+// ----------------------------------------------------------------- launchers
+// (all stream-ordered on `st`; defined in the .cu files)
+
+// k_fe.cu: finite elements
+void launch_assemble(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
+                     const double c[3], const LevDev& L, double* coef,
+                     unsigned long long* bad, cudaStream_t st);
+void launch_rhs(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
+                const double* u0, double* f, cudaStream_t st);
+void launch_recover(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
+                    const double c[3], const double* lam, const double* u0, double* u,
+                    cudaStream_t st);
+
+// k_mg.cu: multigrid on the stencil
+void launch_nat2int(const LevDev& L, const double* src, double* dst, bool zero_dirichlet,
+                    cudaStream_t st);
+void launch_int2nat(const LevDev& L, const double* src, double* dst, cudaStream_t st);
+void launch_gs_sweep(const LevDev& L, const double* coef, double* lam, const double* f,
+                     cudaStream_t st);
+// y = K x (f == NULL) or y = f - K x; optional block partials of sum y^2
+int launch_apply(const LevDev& L, const double* coef, const double* x, const double* f,
+                 double* y, double* partial, cudaStream_t st);
+void launch_reduce_sum(const double* partial, int n, double* out, cudaStream_t st);
+void launch_norm2_partial(const LevDev& L, const double* v, double* partial, int* nblk,
+                          cudaStream_t st);
+struct MapDev {
+    // per direction d: lo[d][t], co[d][t] over fine indices; pos[d][c] over coarse
+    const int* lo[3];
+    const int* co[3];
+    const int* pos[3];
+};
+void launch_restrict(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* r,
+                     double* fc, cudaStream_t st);
+void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* xc,
+                    double* x, cudaStream_t st);
+void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* coefF,
+                     double* coefC, unsigned int* overflow, cudaStream_t st);
+void launch_export27(const LevDev& L, const double* coef, double* K27, cudaStream_t st);
+void launch_zero_dirichlet(const LevDev& L, double* v, cudaStream_t st);
+void launch_argmin_bottom(const double* Z, int n, double* pval, long long* pidx, int nblk,
+                          cudaStream_t st);
+
+// k_coarse.cu: coarsest-level direct solve
+void launch_dense_build(const LevDev& L, const double* coef, double* A, int nf, cudaStream_t st);
+void coarse_prepare(int nf);
+int gj_invert(double* A, int n, double* scratch, cudaStream_t st);
+void launch_coarse_gemv(const LevDev& L, const double* Ainv, int nf, const double* f,
+                        double* x, cudaStream_t st);
+
+}  // namespace wd
