@@ -233,13 +233,15 @@ def run_ours(args, ws, rank, local):
         ctx, ev, rep, prof, keep = gpu_step(wd, prob, opt, args.tol, stream, host)
         return ctx, ev, rep, prof
 
+    def hier_info(ctx):
+        return ([ctx.level_dims(l) for l in range(ctx.num_levels())],
+                [ctx.level_plan(l) for l in range(ctx.num_levels() - 1)], ctx.device_bytes())
+
     # warm-up
     for _ in range(args.warmup):
         ctx, ev, rep, prof = one()
         torch.cuda.synchronize()
-        levels = [ctx.level_dims(l) for l in range(ctx.num_levels())]
-        plans = [ctx.level_plan(l) for l in range(ctx.num_levels() - 1)]
-        dev_bytes = ctx.device_bytes()
+        info = hier_info(ctx)
         ctx.close()
     # timed region
     barrier(ws)
@@ -260,10 +262,12 @@ def run_ours(args, ws, rank, local):
             gs_sweeps += int(prof["gs0_sweeps"])
             vc_ms += prof["vcycle_ms"]
             vc_n += int(prof["vcycles"])
+            info = hier_info(ctx)
             ctx.close()   # frees device memory; ordered after the step's work
         stop.record(stream)
         torch.cuda.synchronize()
     launches = wd.wd_launch_count() - l0
+    levels, plans, dev_bytes = info
     barrier(ws)
     ms_total = max_over_ranks(ws, start.elapsed_time(stop))
     ms_step = ms_total / args.steps

@@ -308,9 +308,9 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st) {
     const bool prof = ctx->opt.profile && l == 0;
     int ns = 0;
     for (int s = 0; s < ctx->opt.pre_smooth; s++, ns++) {
-        if (prof && ns < 16) CK(cudaEventRecord(ctx->ev_gs[2 * ns], st));
+        if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns], st, cudaEventRecordExternal));
         launch_gs_sweep(F.L, F.coef, F.lam, F.f, st);
-        if (prof && ns < 16) CK(cudaEventRecord(ctx->ev_gs[2 * ns + 1], st));
+        if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns + 1], st, cudaEventRecordExternal));
     }
     launch_apply(F.L, F.coef, F.lam, F.f, F.r, nullptr, st);
     launch_restrict(F.L, C.L, F.M, F.r, C.f, st);
@@ -320,9 +320,9 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st) {
     if (rc) return rc;
     launch_prolong(F.L, C.L, F.M, C.lam, F.lam, st);
     for (int s = 0; s < ctx->opt.post_smooth; s++, ns++) {
-        if (prof && ns < 16) CK(cudaEventRecord(ctx->ev_gs[2 * ns], st));
+        if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns], st, cudaEventRecordExternal));
         launch_gs_sweep(F.L, F.coef, F.lam, F.f, st);
-        if (prof && ns < 16) CK(cudaEventRecord(ctx->ev_gs[2 * ns + 1], st));
+        if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns + 1], st, cudaEventRecordExternal));
     }
     CKL();
     return WD_OK;

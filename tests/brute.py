@@ -46,6 +46,45 @@ def free_mask(shape):
     return m
 
 
+def _shift_slices(n, d):
+    """slices (src, dst) so that dst index t corresponds to src index t + d."""
+    if d >= 0:
+        return slice(d, n), slice(0, n - d)
+    return slice(0, n + d), slice(-d, n)
+
+
+def neighbour_view(a, dx, dy, dz, fill=0):
+    """b[k,j,i] = a[k+dz, j+dy, i+dx] (fill outside the grid)."""
+    n3, n2, n1 = a.shape[:3]
+    b = np.full_like(a, fill)
+    sx, tx = _shift_slices(n1, dx)
+    sy, ty = _shift_slices(n2, dy)
+    sz, tz = _shift_slices(n3, dz)
+    b[tz, ty, tx] = a[sz, sy, sx]
+    return b
+
+
+def free_pair_mask(shape):
+    """(n3,n2,n1,27) mask of couplings K[p, o] with both p and p + d_o free."""
+    fm = free_mask(shape)
+    m = np.zeros(shape + (27,), dtype=bool)
+    for o in range(27):
+        dx, dy, dz = o % 3 - 1, (o // 3) % 3 - 1, o // 9 - 1
+        m[..., o] = fm & neighbour_view(fm, dx, dy, dz, False)
+    return m
+
+
+def stencil_asymmetry(K):
+    """max |K[p, o] - K[p + d_o, 26 - o]| over in-grid pairs."""
+    worst = 0.0
+    for o in range(27):
+        dx, dy, dz = o % 3 - 1, (o // 3) % 3 - 1, o // 9 - 1
+        other = neighbour_view(K[..., 26 - o], dx, dy, dz, np.nan)
+        d = np.abs(K[..., o] - other)
+        worst = max(worst, float(np.nanmax(d)) if np.isfinite(d).any() else 0.0)
+    return worst
+
+
 def fast_diag_solve(hx, hy, hz, c, f):
     """lambda* = K_FF^{-1} f_F on a flat box by fast diagonalisation: 1-D
     generalised eigenproblems S v = mu M v restricted to the free index set of

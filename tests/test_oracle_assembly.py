@@ -172,3 +172,14 @@ def test_validate_mesh_reports_lowest_bad_element():
     e, what = oracle.validate_mesh(X, Y, Z)
     # the inverted edge lies in elements (6..7, 4..5, 3); lowest is (6,4,3)
     assert e == (3 * 16 + 4) * 16 + 6 and what == 0
+
+
+def test_stencil_asymmetry_helper():
+    """The shifted-array symmetry check used on large GPU stencils agrees with
+    the dense check: 0 on the oracle's assembled K, > 0 once perturbed."""
+    from brute import stencil_asymmetry
+    p = synth.tiny()
+    K = oracle.assemble(*_np(p)[:3], (1, 1, 2))
+    assert stencil_asymmetry(K) == 0.0
+    K[3, 4, 5, 14] += 1e-9
+    assert stencil_asymmetry(K) > 0
