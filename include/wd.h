@@ -177,6 +177,13 @@ void wd_profile_reset(wd_ctx* ctx);
 /* Cumulative number of kernel launches executed by this library in this
  * process (a CUDA-graph replay counts its kernel nodes). */
 long long wd_launch_count(void);
+/* Time one internal kernel (or step) on the context's own buffers with CUDA
+ * events: which = 0 GS sweep (4 colour phases), 1 residual apply, 2 restrict
+ * (level -> level+1), 3 prolong, 4 V-cycle (level 0), 5 residual norm
+ * (level 0), 6 Galerkin (level -> level+1), 7 level-0 assembly.  One untimed
+ * warm-up, then *ms_out = mean over `reps`.  Overwrites internal vectors
+ * (and, for 6/7, recomputes identical operators). */
+int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out);
 
 #ifdef __cplusplus
 }

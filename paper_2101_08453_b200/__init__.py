@@ -87,13 +87,18 @@ _lib.wd_residual_norm.argtypes = [_vp, _dp, _dp, C.POINTER(C.c_double),
 _lib.wd_profile_read.argtypes = [_vp, C.POINTER(C.c_double), C.c_int]
 _lib.wd_profile_reset.argtypes = [_vp]
 _lib.wd_launch_count.restype = C.c_longlong
+_lib.wd_bench_kernel.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
 
 # every symbol include/wd.h declares
 ABI_SYMBOLS = ["wd_default_options", "wd_assemble", "wd_rhs", "wd_vcycle", "wd_solve",
                "wd_recover_wind", "wd_destroy", "wd_last_error", "wd_device_bytes",
                "wd_num_levels", "wd_level_dims", "wd_level_plan", "wd_get_stencil",
                "wd_apply", "wd_smooth", "wd_restrict", "wd_prolong", "wd_coarse_solve",
-               "wd_residual_norm", "wd_profile_read", "wd_profile_reset", "wd_launch_count"]
+               "wd_residual_norm", "wd_profile_read", "wd_profile_reset", "wd_launch_count",
+               "wd_bench_kernel"]
+
+BENCH_KERNELS = {"gs_sweep": 0, "apply": 1, "restrict": 2, "prolong": 3, "vcycle": 4,
+                 "residual_norm": 5, "galerkin": 6, "assemble": 7}
 
 
 class WDError(RuntimeError):
@@ -196,6 +201,13 @@ def wd_profile_reset(ctx: Context):
 
 def wd_launch_count() -> int:
     return int(_lib.wd_launch_count())
+
+
+def wd_bench_kernel(ctx: Context, which, level=0, reps=10) -> float:
+    ms = C.c_double()
+    w = BENCH_KERNELS[which] if isinstance(which, str) else int(which)
+    _check(_lib.wd_bench_kernel(ctx.h, w, level, reps, C.byref(ms)))
+    return ms.value
 
 
 # ------------------------------------------------------------------ ABI calls

@@ -20,7 +20,8 @@ namespace wd {
 namespace {
 
 constexpr int GS_BLK = 128;
-constexpr int AP_BLK = 128;
+constexpr int AP_ROWS = 4;
+constexpr int AP_BLK = 64 * AP_ROWS;
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
@@ -113,24 +114,36 @@ __device__ __forceinline__ double block_sum(double v) {
     __shared__ double ws[32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int w = tid >> 5, l = tid & 31;
     if (l == 0) ws[w] = v;
     __syncthreads();
     double r = 0.0;
-    if (threadIdx.x == 0) {
-        const int nw = (blockDim.x + 31) >> 5;
+    if (tid == 0) {
+        const int nw = (blockDim.x * blockDim.y * blockDim.z + 31) >> 5;
         for (int t = 0; t < nw; t++) r += ws[t];
     }
     __syncthreads();
     return r;
 }
 
+// CTA = 32 half-row positions x 2 parities x AP_ROWS rows: the backward
+// couplings of a node (stored at the neighbour) are mostly loaded by another
+// thread of the same CTA in the same or the previous k step (L1/L2 reuse).
 __global__ void __launch_bounds__(AP_BLK)
 apply_kernel(LevDev L, const double* __restrict__ K, const double* __restrict__ x,
-             const double* __restrict__ f, double* __restrict__ y, double* __restrict__ partial) {
-    const int a = blockIdx.x * AP_BLK + threadIdx.x;
-    const int j = blockIdx.y;
-    const int ci = blockIdx.z;
+             const double* __restrict__ f, double* __restrict__ y, double* __restrict__ partial,
+             int variant) {
+    int a, ci, j;
+    if (variant == 0) {          // 128 along the half row, parity in blockIdx.z
+        a = blockIdx.x * 128 + threadIdx.x; ci = blockIdx.z; j = blockIdx.y;
+    } else if (variant == 1) {   // 128 along the half row, parity interleaved in blockIdx.x
+        a = (blockIdx.x >> 1) * 128 + threadIdx.x; ci = blockIdx.x & 1; j = blockIdx.y;
+    } else if (variant == 2) {   // 32 x 2 parities x AP_ROWS rows
+        a = blockIdx.x * 32 + threadIdx.x; ci = threadIdx.y; j = blockIdx.y * AP_ROWS + threadIdx.z;
+    } else {                     // 128 x 2 parities, one row
+        a = blockIdx.x * 128 + threadIdx.x; ci = threadIdx.y; j = blockIdx.y;
+    }
     const int i = 2 * a + ci;
     double acc = 0.0;
     if (i >= 1 && i <= L.n1 - 2 && j >= 1 && j <= L.n2 - 2) {
@@ -165,8 +178,8 @@ apply_kernel(LevDev L, const double* __restrict__ K, const double* __restrict__ 
     }
     if (partial) {
         const double s = block_sum(acc);
-        if (threadIdx.x == 0)
-            partial[((i64)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
+        if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0)
+            partial[(i64)blockIdx.y * gridDim.x + blockIdx.x] = s;
     }
 }
 
@@ -418,9 +431,14 @@ void launch_gs_sweep(const LevDev& L, const double* coef, double* lam, const dou
 int launch_apply(const LevDev& L, const double* coef, const double* x, const double* f, double* y,
                  double* partial, cudaStream_t st) {
     const int half = (L.n1 + 1) / 2;
-    dim3 grid((half + AP_BLK - 1) / AP_BLK, L.n2, 2);
+    const int v = g_apply_variant;
+    dim3 grid, blk;
+    if (v == 0) { grid = dim3((half + 127) / 128, L.n2, 2); blk = dim3(128); }
+    else if (v == 1) { grid = dim3(2 * ((half + 127) / 128), L.n2, 1); blk = dim3(128); }
+    else if (v == 2) { grid = dim3((half + 31) / 32, (L.n2 + AP_ROWS - 1) / AP_ROWS, 1); blk = dim3(32, 2, AP_ROWS); }
+    else { grid = dim3((half + 127) / 128, L.n2, 1); blk = dim3(128, 2); }
     g_launches += 1;
-    apply_kernel<<<grid, AP_BLK, 0, st>>>(L, coef, x, f, y, partial);
+    apply_kernel<<<grid, blk, 0, st>>>(L, coef, x, f, y, partial, v);
     return (int)(grid.x * grid.y * grid.z);
 }
 

@@ -57,7 +57,7 @@ LevDev make_level(int n1, int n2, int n3) {
     L.n2 = n2;
     L.n3 = n3;
     int half = (n1 + 1) / 2;
-    L.H = (half + 15) / 16 * 16;
+    L.H = std::max((half + 15) / 16 * 16, 48);   // >= the TMA box width (34)
     L.P = 2 * L.H;
     L.plane = (i64)n2 * L.P;
     L.NT = (i64)n3 * L.plane;
@@ -72,13 +72,25 @@ struct Level {
     double* lam = nullptr;
     double* f = nullptr;
     double* r = nullptr;
+    double* raw[4] = {nullptr, nullptr, nullptr, nullptr};   // allocations (with front guard)
     // transition to level + 1
     int hflag = 0;
     int nkept = 0;
     int kept[MAXNZ];
     int* dmap = nullptr;      // device: lo/co/pos for 3 directions
     MapDev M;
+    // TMA tensor maps (CUtensorMap, 128 B each): coefficient slots 0-4 and 5-13,
+    // x = lam (halo box) and f (tile box) of this level
+    alignas(64) unsigned char tmA[128], tmB[128], tmX[128], tmF[128];
 };
+
+// residual r = f - K lam (f_on) or r = K lam on level `lv`; optional per-CTA partials
+int apply_level(Level& lv, bool f_on, double* partial, cudaStream_t st) {
+    if (g_apply_variant >= 0)
+        return launch_apply_tma(lv.L, lv.tmA, lv.tmB, lv.tmX, f_on ? lv.tmF : nullptr, lv.r,
+                                partial, st);
+    return launch_apply(lv.L, lv.coef, lv.lam, f_on ? lv.f : nullptr, lv.r, partial, st);
+}
 
 }  // namespace
 
@@ -112,21 +124,46 @@ struct wd_ctx {
 
 namespace wd {
 std::atomic<long long> g_launches{0};
+int g_apply_variant = 1;
 }
 
 namespace {
 
+// Device allocations come from the device's default stream-ordered memory pool
+// with an unlimited release threshold, so a context built after another one
+// was destroyed reuses the retained memory instead of remapping it.
+void ensure_pool() {
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done[dev] = true;
+}
+
 int dalloc(wd_ctx* ctx, void** p, size_t bytes) {
-    cudaError_t e = cudaMalloc(p, bytes > 0 ? bytes : 8);
+    ensure_pool();
+    const size_t b = bytes > 0 ? bytes : 8;
+    cudaError_t e = cudaMallocAsync(p, b, 0);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(e == cudaErrorMemoryAllocation ? WD_E_OOM : WD_E_CUDA,
-                    "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+                    "cudaMallocAsync(%zu) failed: %s", bytes, cudaGetErrorString(e));
     }
     if (ctx) ctx->bytes += (long long)bytes;
-    e = cudaMemset(*p, 0, bytes > 0 ? bytes : 8);
+    e = cudaMemsetAsync(*p, 0, b, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
     if (e != cudaSuccess) return fail(WD_E_CUDA, "cudaMemset failed: %s", cudaGetErrorString(e));
     return WD_OK;
+}
+
+void dfree(void* p) {
+    if (p) cudaFreeAsync(p, 0);
 }
 
 bool is_device_ptr(const void* p) {
@@ -214,7 +251,7 @@ int stage_finish(cudaStream_t st, std::initializer_list<Stage*> list) {
     for (Stage* s : list) {
         if (!s->staged) continue;
         if (s->ctx && s->slot >= 0) s->ctx->pool_busy[s->slot] = 0;
-        if (s->own) cudaFree(s->own);
+        if (s->own) dfree(s->own);
         s->staged = false;
     }
     return WD_OK;
@@ -281,10 +318,16 @@ int alloc_level(wd_ctx* ctx, Level& lv, int n1, int n2, int n3) {
     lv.L = make_level(n1, n2, n3);
     const size_t nt = (size_t)lv.L.NT;
     int rc;
-    if ((rc = dalloc(ctx, (void**)&lv.coef, sizeof(double) * 14 * nt))) return rc;
-    if ((rc = dalloc(ctx, (void**)&lv.lam, sizeof(double) * nt))) return rc;
-    if ((rc = dalloc(ctx, (void**)&lv.f, sizeof(double) * nt))) return rc;
-    if ((rc = dalloc(ctx, (void**)&lv.r, sizeof(double) * nt))) return rc;
+    const size_t g = 0;   // front guard (doubles) before each array
+    double** arr[4] = {&lv.coef, &lv.lam, &lv.f, &lv.r};
+    const size_t len[4] = {14 * nt, nt, nt, nt};
+    for (int t = 0; t < 4; t++) {
+        if ((rc = dalloc(ctx, (void**)&lv.raw[t], sizeof(double) * (len[t] + g)))) return rc;
+        *arr[t] = lv.raw[t] + g;
+    }
+    if (make_coef_maps(lv.L, lv.coef, lv.tmA, lv.tmB) || make_vec_map(lv.L, lv.lam, lv.tmX, true) ||
+        make_vec_map(lv.L, lv.f, lv.tmF, false))
+        return fail(WD_E_CUDA, "cuTensorMapEncodeTiled failed for level dims (%d,%d,%d)", n1, n2, n3);
     return WD_OK;
 }
 
@@ -312,7 +355,7 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st) {
         launch_gs_sweep(F.L, F.coef, F.lam, F.f, st);
         if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns + 1], st, cudaEventRecordExternal));
     }
-    launch_apply(F.L, F.coef, F.lam, F.f, F.r, nullptr, st);
+    apply_level(F, true, nullptr, st);
     launch_restrict(F.L, C.L, F.M, F.r, C.f, st);
     CK(cudaMemsetAsync(C.lam, 0, sizeof(double) * C.L.NT, st));
     CKL();
@@ -384,7 +427,7 @@ int run_vcycle(wd_ctx* ctx, cudaStream_t st) {
 int residual_sq(wd_ctx* ctx, int slot, cudaStream_t st) {
     Level& F = ctx->lev[0];
     if (ctx->opt.profile) CK(cudaEventRecord(ctx->ev_res[0], st));
-    int nb = launch_apply(F.L, F.coef, F.lam, F.f, F.r, ctx->partial, st);
+    int nb = apply_level(F, true, ctx->partial, st);
     launch_reduce_sum(ctx->partial, nb, ctx->dscal + slot, st);
     if (ctx->opt.profile) CK(cudaEventRecord(ctx->ev_res[1], st));
     CKL();
@@ -434,6 +477,8 @@ const char* wd_last_error(void) { return g_err; }
 
 void wd_destroy(wd_ctx* ctx) {
     if (!ctx) return;
+    cudaDeviceSynchronize();   // no work of the context may still be in flight
+    cudaGetLastError();
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
     if (ctx->cap) cudaStreamDestroy(ctx->cap);
     for (auto e : ctx->ev_gs) if (e) cudaEventDestroy(e);
@@ -441,21 +486,18 @@ void wd_destroy(wd_ctx* ctx) {
     for (auto e : ctx->ev_res) if (e) cudaEventDestroy(e);
     for (int l = 0; l < ctx->nlev; l++) {
         Level& lv = ctx->lev[l];
-        cudaFree(lv.coef);
-        cudaFree(lv.lam);
-        cudaFree(lv.f);
-        cudaFree(lv.r);
-        cudaFree(lv.dmap);
+        for (double* p : lv.raw) dfree(p);
+        dfree(lv.dmap);
     }
-    cudaFree(ctx->X);
-    cudaFree(ctx->Y);
-    cudaFree(ctx->Z);
-    cudaFree(ctx->Ainv);
-    cudaFree(ctx->Dinv);
-    cudaFree(ctx->partial);
-    cudaFree(ctx->dscal);
+    dfree(ctx->X);
+    dfree(ctx->Y);
+    dfree(ctx->Z);
+    dfree(ctx->Ainv);
+    dfree(ctx->Dinv);
+    dfree(ctx->partial);
+    dfree(ctx->dscal);
     if (ctx->hscal) cudaFreeHost(ctx->hscal);
-    for (auto& p : ctx->pool) cudaFree(p.first);
+    for (auto& p : ctx->pool) dfree(p.first);
     delete ctx;
 }
 
@@ -491,6 +533,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
     if ((rc = dalloc(ctx, (void**)&ctx->dscal, sizeof(double) * 4096))) return rc;
     CK(cudaMallocHost((void**)&ctx->hscal, sizeof(double) * 64));
     CK(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
+    apply_tma_prepare();
     if (ctx->opt.profile) {
         for (auto& e : ctx->ev_gs) CK(cudaEventCreate(&e));
         for (auto& e : ctx->ev_cyc) CK(cudaEventCreate(&e));
@@ -620,6 +663,8 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
                 wd_ctx** out) {
     if (!out) return fail(WD_E_INVAL, "out is NULL");
     *out = nullptr;
+    if (const char* v = getenv("WD_APPLY_VARIANT")) g_apply_variant = atoi(v);
+    if (const char* v = getenv("WD_TMA_DEBUG")) g_tma_debug = atoi(v);
     if (!X || !Y || !Z) return fail(WD_E_INVAL, "NULL coordinate array");
     if (n1 < 3 || n2 < 3 || n3 < 2) return fail(WD_E_INVAL, "dims (%d,%d,%d): need n1,n2 >= 3, n3 >= 2", n1, n2, n3);
     if (n3 - 1 >= MAXNZ) return fail(WD_E_INVAL, "n3 = %d exceeds %d", n3, MAXNZ);
@@ -791,6 +836,51 @@ void wd_profile_reset(wd_ctx* ctx) {
 
 long long wd_launch_count(void) { return g_launches.load(); }
 
+int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out) {
+    int rc = check_level(ctx, level);
+    if (rc) return rc;
+    if (reps < 1 || !ms_out) return fail(WD_E_INVAL, "reps < 1 or NULL output");
+    if ((which == 2 || which == 3 || which == 6) && level >= ctx->nlev - 1)
+        return fail(WD_E_INVAL, "no coarser level");
+    cudaStream_t st = ctx->cap;
+    Level& F = ctx->lev[level];
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    auto body = [&]() -> int {
+        switch (which) {
+            case 0: launch_gs_sweep(F.L, F.coef, F.lam, F.f, st); break;
+            case 1: apply_level(F, true, nullptr, st); break;
+            case 2: launch_restrict(F.L, ctx->lev[level + 1].L, F.M, F.r, ctx->lev[level + 1].f, st); break;
+            case 3: launch_prolong(F.L, ctx->lev[level + 1].L, F.M, ctx->lev[level + 1].lam, F.lam, st); break;
+            case 4: return run_vcycle(ctx, st);
+            case 5: return residual_sq(ctx, 0, st);
+            case 6: launch_galerkin(F.L, ctx->lev[level + 1].L, F.M, F.coef, ctx->lev[level + 1].coef, nullptr, st); break;
+            case 7: {
+                unsigned long long* dbad = (unsigned long long*)(ctx->dscal + 8);
+                launch_assemble(ctx->X, ctx->Y, ctx->Z, ctx->n1, ctx->n2, ctx->n3, ctx->c,
+                                ctx->lev[0].L, ctx->lev[0].coef, dbad, st);
+                break;
+            }
+            default: return fail(WD_E_INVAL, "unknown kernel %d", which);
+        }
+        return WD_OK;
+    };
+    if ((rc = body())) return rc;   // warm-up
+    CK(cudaEventRecord(e0, st));
+    for (int r = 0; r < reps; r++)
+        if ((rc = body())) return rc;
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_out = ms / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CKL();
+    return WD_OK;
+}
+
 // ------------------------------------------------------------------ inspection
 int wd_num_levels(const wd_ctx* ctx) { return ctx ? ctx->nlev : 0; }
 
@@ -835,7 +925,7 @@ int wd_apply(wd_ctx* ctx, int level, const double* x, double* y, void* stream) {
     if ((rc = stage_in(ctx, sx, x, N, st)) || (rc = stage_out(ctx, sy, y, N))) return rc;
     launch_nat2int(lv.L, sx.d, lv.lam, true, st);
     CK(cudaMemsetAsync(lv.r, 0, sizeof(double) * lv.L.NT, st));
-    launch_apply(lv.L, lv.coef, lv.lam, nullptr, lv.r, nullptr, st);
+    apply_level(lv, false, nullptr, st);
     launch_int2nat(lv.L, lv.r, sy.d, st);
     CKL();
     return stage_finish(st, {&sx, &sy});

@@ -22,6 +22,9 @@ namespace wd {
 // kernels launched by this library (defined in wd_api.cu); launchers add the
 // number of kernels they enqueue
 extern std::atomic<long long> g_launches;
+// development knob: thread mapping of apply_kernel (env WD_APPLY_VARIANT)
+extern int g_apply_variant;
+extern int g_tma_debug;
 
 typedef long long i64;
 
@@ -96,6 +99,13 @@ void launch_export27(const LevDev& L, const double* coef, double* K27, cudaStrea
 void launch_zero_dirichlet(const LevDev& L, double* v, cudaStream_t st);
 void launch_argmin_bottom(const double* Z, int n, double* pval, long long* pidx, int nblk,
                           cudaStream_t st);
+
+// k_apply_tma.cu: TMA-staged residual / apply
+int make_coef_maps(const LevDev& L, const double* coef, void* mapA, void* mapB);
+int make_vec_map(const LevDev& L, const double* v, void* map, bool halo);
+void apply_tma_prepare();
+int launch_apply_tma(const LevDev& L, const void* mapA, const void* mapB, const void* mapX,
+                     const void* mapF, double* y, double* partial, cudaStream_t st);
 
 // k_coarse.cu: coarsest-level direct solve
 void launch_dense_build(const LevDev& L, const double* coef, double* A, int nf, cudaStream_t st);

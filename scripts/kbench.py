@@ -1,0 +1,65 @@
+#!/usr/bin/env python
+"""Per-kernel timing (CUDA events, through wd_bench_kernel) on a config, with
+algorithmic bytes -> GB/s.  Development tool; prints one JSON line per kernel.
+
+  python scripts/kbench.py [--config paper] [--reps 10] [--apply-variants 0,1,2,3]
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="paper")
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--apply-variants", default="")
+    args = ap.parse_args()
+    import paper_2101_08453_b200 as wd
+    import synth
+    dev = torch.device("cuda:0")
+    p = synth.make(args.config, device=dev)
+    ctx = wd.wd_assemble(p.X, p.Y, p.Z, p.a)
+    f = wd.wd_rhs(ctx, p.u0)
+    lam, rep = wd.wd_solve(ctx, f, rel_tol=1e-8)
+    n1, n2, n3 = ctx.level_dims(0)
+    free0 = (n1 - 2) * (n2 - 2) * (n3 - 1)
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    alg = {"gs_sweep": 264 * free0, "apply": 136 * free0, "residual_norm": 128 * free0,
+           "prolong": 16 * free0, "restrict": 8 * free0 + 8 * free0 // 4}
+
+    def report(name, level=0, extra=None):
+        ms = wd.wd_bench_kernel(ctx, name, level, args.reps)
+        d = {"kernel": name, "level": level, "ms": ms}
+        if level == 0 and name in alg:
+            gbs = alg[name] / (ms * 1e-3) / 1e9
+            d.update(alg_GBps=gbs, frac=gbs / peak)
+        if extra:
+            d.update(extra)
+        print(json.dumps(d), flush=True)
+
+    for name in ["gs_sweep", "apply", "residual_norm", "restrict", "prolong", "vcycle"]:
+        report(name)
+    for l in range(1, ctx.num_levels() - 1):
+        report("gs_sweep", l)
+    report("assemble")
+    for l in range(ctx.num_levels() - 1):
+        report("galerkin", l)
+    if args.apply_variants:
+        tiny = synth.tiny(device=dev)
+        for v in args.apply_variants.split(","):
+            os.environ["WD_APPLY_VARIANT"] = v
+            wd.wd_assemble(tiny.X, tiny.Y, tiny.Z, tiny.a).close()   # re-reads the knob
+            report("apply", 0, {"variant": int(v)})
+    print(json.dumps({"levels": [ctx.level_dims(l) for l in range(ctx.num_levels())],
+                      "cycles": rep["cycles"], "device_bytes": ctx.device_bytes()}))
+
+
+if __name__ == "__main__":
+    main()
