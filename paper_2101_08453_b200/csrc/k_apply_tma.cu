@@ -298,7 +298,7 @@ int make_coef_maps(const LevDev& L, const double* coef, void* mapA, void* mapB) 
     auto enc = encode_fn();
     if (!enc) return -1;
     cuuint64_t dims[5] = {(cuuint64_t)L.H, 2, (cuuint64_t)L.n2, (cuuint64_t)L.n3, 14};
-    cuuint64_t str[4] = {(cuuint64_t)L.H * 8, (cuuint64_t)L.P * 8, (cuuint64_t)L.plane * 8,
+    cuuint64_t str[4] = {(cuuint64_t)L.H * 8, (cuuint64_t)L.sj * 8, (cuuint64_t)L.sk * 8,
                          (cuuint64_t)L.NT * 8};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
     cuuint32_t boxA[5] = {BP, 2, A_ROWS, 1, 5};
@@ -320,7 +320,7 @@ int make_vec_map(const LevDev& L, const double* v, void* map, bool halo) {
     auto enc = encode_fn();
     if (!enc) return -1;
     cuuint64_t dims[4] = {(cuuint64_t)L.H, 2, (cuuint64_t)L.n2, (cuuint64_t)L.n3};
-    cuuint64_t str[3] = {(cuuint64_t)L.H * 8, (cuuint64_t)L.P * 8, (cuuint64_t)L.plane * 8};
+    cuuint64_t str[3] = {(cuuint64_t)L.H * 8, (cuuint64_t)L.sj * 8, (cuuint64_t)L.sk * 8};
     cuuint32_t es[4] = {1, 1, 1, 1};
     cuuint32_t boxX[4] = {BP, 2, X_ROWS, 1};
     cuuint32_t boxF[4] = {TI, 2, TJ, 1};

@@ -32,9 +32,9 @@ __device__ __forceinline__ void column_offsets(const LevDev& L, int ci, i64 (&co
     const i64 xp = ci ? 1 - (i64)L.H : (i64)L.H;    // i+1
 #pragma unroll
     for (int oy = -1; oy <= 1; oy++) {
-        co[0 + 3 * (oy + 1)] = (i64)oy * L.P + xm;
-        co[1 + 3 * (oy + 1)] = (i64)oy * L.P;
-        co[2 + 3 * (oy + 1)] = (i64)oy * L.P + xp;
+        co[0 + 3 * (oy + 1)] = (i64)oy * L.sj + xm;
+        co[1 + 3 * (oy + 1)] = (i64)oy * L.sj;
+        co[2 + 3 * (oy + 1)] = (i64)oy * L.sj + xp;
     }
 }
 
@@ -61,7 +61,7 @@ __device__ __forceinline__ double offdiag(const LevDev& L, const double* __restr
         const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
         if (dz) {
             if (has_below) {
-                const double kv = ldg(K + sl * NT + base - L.plane + co[cidx(-dx, -dy)]);
+                const double kv = ldg(K + sl * NT + base - L.sk + co[cidx(-dx, -dy)]);
                 s = fma(kv, xm[cidx(-dx, -dy)], s);
             }
         } else {
@@ -87,11 +87,11 @@ gs_phase_kernel(LevDev L, const double* __restrict__ K, double* lam,
     for (int c = 0; c < 9; c++) {
         xm[c] = 0.0;
         x0[c] = c == 4 ? lam[own] : ldg(lam + own + co[c]);
-        xp[c] = c == 4 ? lam[own + L.plane] : ldg(lam + own + L.plane + co[c]);
+        xp[c] = c == 4 ? lam[own + L.sk] : ldg(lam + own + L.sk + co[c]);
     }
     const int kt = L.n3 - 2;   // top free level
     for (int k = 0; k <= kt; k++) {
-        const i64 base = own + (i64)k * L.plane;
+        const i64 base = own + (i64)k * L.sk;
         const double s = offdiag(L, K, base, co, xm, x0, xp, k > 0);
         const double v = (ldg(f + base) - s) / ldg(K + base);
         lam[base] = v;
@@ -102,7 +102,7 @@ gs_phase_kernel(LevDev L, const double* __restrict__ K, double* lam,
             x0[c] = xp[c];
         }
         if (k + 2 <= L.n3 - 1) {
-            const i64 nb = base + 2 * L.plane;
+            const i64 nb = base + 2 * L.sk;
 #pragma unroll
             for (int c = 0; c < 9; c++) xp[c] = c == 4 ? lam[nb] : ldg(lam + nb + co[c]);
         }
@@ -155,10 +155,10 @@ apply_kernel(LevDev L, const double* __restrict__ K, const double* __restrict__ 
         for (int c = 0; c < 9; c++) {
             xm[c] = 0.0;
             x0[c] = ldg(x + own + co[c]);
-            xp[c] = ldg(x + own + L.plane + co[c]);
+            xp[c] = ldg(x + own + L.sk + co[c]);
         }
         for (int k = 0; k <= L.n3 - 2; k++) {
-            const i64 base = own + (i64)k * L.plane;
+            const i64 base = own + (i64)k * L.sk;
             double s = offdiag(L, K, base, co, xm, x0, xp, k > 0);
             s = fma(ldg(K + base), x0[4], s);
             const double v = f ? ldg(f + base) - s : s;
@@ -170,7 +170,7 @@ apply_kernel(LevDev L, const double* __restrict__ K, const double* __restrict__ 
                 x0[c] = xp[c];
             }
             if (k + 2 <= L.n3 - 1) {
-                const i64 nb = base + 2 * L.plane;
+                const i64 nb = base + 2 * L.sk;
 #pragma unroll
                 for (int c = 0; c < 9; c++) xp[c] = ldg(x + nb + co[c]);
             }

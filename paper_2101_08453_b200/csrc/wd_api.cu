@@ -59,8 +59,9 @@ LevDev make_level(int n1, int n2, int n3) {
     int half = (n1 + 1) / 2;
     L.H = std::max((half + 15) / 16 * 16, 48);   // >= the TMA box width (34)
     L.P = 2 * L.H;
-    L.plane = (i64)n2 * L.P;
-    L.NT = (i64)n3 * L.plane;
+    L.sk = L.P;
+    L.sj = (i64)n3 * L.P;
+    L.NT = (i64)n2 * L.sj;
     return L;
 }
 

@@ -28,14 +28,17 @@ extern int g_tma_debug;
 
 typedef long long i64;
 
+// Row-outer layout [j][k][half][pos]: one node row of all levels (n3 * P
+// doubles) is contiguous, so a slab halo row is a single block to copy/send.
 struct LevDev {
     int n1, n2, n3;
-    int H, P;
-    i64 plane, NT;
+    int H, P;      // half-row pitch, row pitch (2H)
+    i64 sk, sj;    // strides of k (= P) and of j (= n3 P)
+    i64 NT;        // entries per array (= n2 sj)
 };
 
 __host__ __device__ __forceinline__ i64 loff(const LevDev& L, int i, int j, int k) {
-    return (i64)k * L.plane + (i64)j * L.P + (i64)((i & 1) * L.H + (i >> 1));
+    return (i64)j * L.sj + (i64)k * L.sk + (i64)((i & 1) * L.H + (i >> 1));
 }
 
 // forward offsets of the 14 slots (slot 0 = diagonal)
