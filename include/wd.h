@@ -70,10 +70,20 @@ typedef struct {
     int coarse_iters;        /* GS sweeps on the coarsest level when it is larger (default 50) */
     int coarsen_rule;        /* WD_RULE_* (default WD_RULE_COUPLING_CUR) */
     int use_graph;           /* capture the V-cycle as a CUDA graph (default 1) */
-    long long gather_below_nodes; /* multi-GPU coarse gather threshold (reserved, default 0) */
-    int rank, nranks;        /* multi-GPU slab decomposition (reserved; 0, 1 on one GPU) */
-    void* nccl_comm;         /* reserved, NULL */
-    int j_begin, j_end;      /* reserved: owned node rows [j_begin, j_end) */
+    long long gather_below_nodes; /* slab decomposition: replicate ("gather") coarse levels with
+                                     fewer nodes than this (default 2,000,000) */
+    int rank, nranks;        /* slab decomposition in node rows j:
+                                nranks = 1: one GPU, whole grid (default);
+                                nranks > 1, rank >= 0: this process is `rank` of nranks (one
+                                  GPU per process, NCCL over NVLink, nccl_comm required); the
+                                  node/element arrays passed to every call are this rank's
+                                  rows [max(j_begin-2,0), min(j_end+2,n2)) (2 halo rows);
+                                nranks > 1, rank = -1: virtual ranks -- the whole grid on this
+                                  GPU split into nranks slabs with the same halo exchanges done
+                                  as device copies (arrays are the whole grid) */
+    void* nccl_comm;         /* ncclComm_t of the nranks processes (wd_nccl_comm_init) */
+    int j_begin, j_end;      /* owned node rows [j_begin, j_end) of this rank; must equal
+                                wd_partition_rows(n2, nranks, rank) */
     int profile;             /* 1: CUDA events around level-0 smoothing and each V-cycle (default 0) */
 } wd_options;
 
@@ -133,8 +143,21 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
 int wd_recover_wind(wd_ctx* ctx, const double* lambda, const double* u0, double* u,
                     void* stream);
 
-/* Free the context and all its device memory (NULL is a no-op). */
+/* Free the context and all its device memory (NULL is a no-op).  The NCCL
+ * communicator passed in the options is not destroyed. */
 void wd_destroy(wd_ctx* ctx);
+
+/* ---- slab decomposition helpers ----
+ * Owned node rows [*j_begin, *j_end) of `rank` among nranks: an even split
+ * floor(n2 r / R) .. floor(n2 (r+1) / R).  Every rank must own >= 4 rows. */
+void wd_partition_rows(int n2, int nranks, int rank, int* j_begin, int* j_end);
+/* ncclGetUniqueId (libnccl.so.2 is loaded at run time) into id[128]; rank 0
+ * calls it and broadcasts the bytes to the other ranks. */
+int wd_nccl_unique_id(char id[128]);
+/* ncclCommInitRank; *comm receives the ncclComm_t for wd_options.nccl_comm. */
+int wd_nccl_comm_init(const char id[128], int nranks, int rank, void** comm);
+/* First replicated (gathered) level of a decomposed context, -1 if none. */
+int wd_gather_level(const wd_ctx* ctx);
 
 /* Thread-local message of the last failing call ("" if none). */
 const char* wd_last_error(void);

@@ -88,6 +88,10 @@ _lib.wd_profile_read.argtypes = [_vp, C.POINTER(C.c_double), C.c_int]
 _lib.wd_profile_reset.argtypes = [_vp]
 _lib.wd_launch_count.restype = C.c_longlong
 _lib.wd_bench_kernel.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+_lib.wd_partition_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+_lib.wd_nccl_unique_id.argtypes = [C.c_char_p]
+_lib.wd_nccl_comm_init.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+_lib.wd_gather_level.argtypes = [_vp]
 
 # every symbol include/wd.h declares
 ABI_SYMBOLS = ["wd_default_options", "wd_assemble", "wd_rhs", "wd_vcycle", "wd_solve",
@@ -95,7 +99,8 @@ ABI_SYMBOLS = ["wd_default_options", "wd_assemble", "wd_rhs", "wd_vcycle", "wd_s
                "wd_num_levels", "wd_level_dims", "wd_level_plan", "wd_get_stencil",
                "wd_apply", "wd_smooth", "wd_restrict", "wd_prolong", "wd_coarse_solve",
                "wd_residual_norm", "wd_profile_read", "wd_profile_reset", "wd_launch_count",
-               "wd_bench_kernel"]
+               "wd_bench_kernel", "wd_partition_rows", "wd_nccl_unique_id", "wd_nccl_comm_init",
+               "wd_gather_level"]
 
 BENCH_KERNELS = {"gs_sweep": 0, "apply": 1, "restrict": 2, "prolong": 3, "vcycle": 4,
                  "residual_norm": 5, "galerkin": 6, "assemble": 7}
@@ -208,6 +213,45 @@ def wd_bench_kernel(ctx: Context, which, level=0, reps=10) -> float:
     w = BENCH_KERNELS[which] if isinstance(which, str) else int(which)
     _check(_lib.wd_bench_kernel(ctx.h, w, level, reps, C.byref(ms)))
     return ms.value
+
+
+def wd_partition_rows(n2, nranks, rank):
+    """Owned node rows [j_begin, j_end) of `rank` (even split, wd.h)."""
+    a, b = C.c_int(), C.c_int()
+    _lib.wd_partition_rows(int(n2), int(nranks), int(rank), C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+def slab_rows(n2, nranks, rank, halo=2):
+    """Rows [lo, hi) of the arrays a rank passes in NCCL mode (owned + halo)."""
+    a, b = wd_partition_rows(n2, nranks, rank)
+    return max(a - halo, 0), min(b + halo, n2)
+
+
+def wd_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.wd_nccl_unique_id(buf))
+    return buf.raw
+
+
+def wd_nccl_comm_init(uid: bytes, nranks, rank):
+    comm = C.c_void_p()
+    _check(_lib.wd_nccl_comm_init(C.c_char_p(uid), int(nranks), int(rank), C.byref(comm)))
+    return comm
+
+
+def nccl_comm_from_torch(group=None):
+    """One communicator per process group: rank 0 draws the unique id, the
+    torch process group broadcasts it (plumbing only)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [wd_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return wd_nccl_comm_init(obj[0], world, rank)
+
+
+def wd_gather_level(ctx: "Context") -> int:
+    return int(_lib.wd_gather_level(ctx.h))
 
 
 # ------------------------------------------------------------------ ABI calls

@@ -157,7 +157,7 @@ apply_tma_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__
     auto tile_of = [&](int it, int& a0, int& j0) {
         const int t = (int)blockIdx.x + it * (int)gridDim.x;
         a0 = (t % T.ntx) * TI;
-        j0 = (t / T.ntx) * TJ;
+        j0 = L.own0 + (t / T.ntx) * TJ;   // tiles cover the owned local rows
     };
     // producer state: next AB step and next X unit to issue
     int pAB = 0, pX = 0;
@@ -209,7 +209,7 @@ apply_tma_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__
         const int rr = tz + (j0 > 0 ? 1 : 0);     // own row in a box
         const int pm = p - 1 + ci, pp = p + ci;   // positions of i-1 and i+1 (half hp)
         const int i = 2 * (a0 + tx) + ci, j = j0 + tz;
-        const bool valid = i >= 1 && i <= L.n1 - 2 && j >= 1 && j <= L.n2 - 2;
+        const bool valid = i >= 1 && i <= L.n1 - 2 && row_free(L, j);
         // x window (box rows rr-1..rr+1 = j-1..j+1)
         auto xat = [&](const double* X, int r, int c) -> double {
             const int ox = c % 3 - 1;
@@ -341,7 +341,7 @@ int launch_apply_tma(const LevDev& L, const void* mapA, const void* mapB, const 
                      const void* mapF, double* y, double* partial, cudaStream_t st) {
     Tiles T;
     T.ntx = ((L.n1 + 1) / 2 + TI - 1) / TI;
-    T.nty = (L.n2 + TJ - 1) / TJ;
+    T.nty = (L.own1 - L.own0 + TJ - 1) / TJ;
     T.ntiles = T.ntx * T.nty;
     T.nk = L.n3 - 1;
     int g = grid_size();

@@ -216,11 +216,13 @@ assemble_kernel(const double* __restrict__ X, const double* __restrict__ Y,
 // ------------------------------------------------------------------ RHS
 // f_p = sum_{e ni p} fe_a(p),  fe_a = -8 detJ(0) gradN_a(0).u0_e
 //     = -detJ(0) sum_d s_ad (Ji(0) u0_e)_d          (dN_a/dxi_d(0) = s_ad/8)
+// Coordinates: the level's local rows; u0 / f: ABI arrays (Nat); f is written
+// on the owned rows only, 0 on the Dirichlet set.
 __global__ void __launch_bounds__(NTH)
 rhs_kernel(const double* __restrict__ X, const double* __restrict__ Y,
-           const double* __restrict__ Z, int n1, int n2, int n3,
-           const double* __restrict__ u0, double* __restrict__ f) {
+           const double* __restrict__ Z, LevDev L, Nat u0, Nat f) {
     __shared__ double fe[8][NTH];
+    const int n1 = L.n1, n2 = L.n2, n3 = L.n3;
     const int t = threadIdx.x;
     const int tx = t % TX, ty = t / TX;
     const int i0 = blockIdx.x * (TX - 1), j0 = blockIdx.y * (TY - 1);
@@ -228,9 +230,10 @@ rhs_kernel(const double* __restrict__ X, const double* __restrict__ Y,
     const int nx = n1 - 1, ny = n2 - 1, nz = n3 - 1;
     const bool ev = ei >= 0 && ei < nx && ej >= 0 && ej < ny;
     const int ni = i0 + tx, nj = j0 + ty;
-    const bool nv = tx < TX - 1 && ty < TY - 1 && ni < n1 && nj < n2;
-    const bool ndir = ni == 0 || ni == n1 - 1 || nj == 0 || nj == n2 - 1;
-    const i64 E = (i64)nx * ny * nz;
+    const bool nv = tx < TX - 1 && ty < TY - 1 && ni < n1 && nj >= L.own0 && nj < L.own1;
+    const bool ndir = ni == 0 || ni == n1 - 1 || row_dirichlet(L, nj);
+    const i64 EC = (i64)nz * u0.n2a * nx;   // one component of the element array
+    double* fo = const_cast<double*>(f.p);
     double x[8][3];
     if (ev) load_plane(X, Y, Z, n1, n2, ei, ej, 0, x, 0);
     double top = 0.0;   // contributions to node level ek from element level ek-1
@@ -238,8 +241,8 @@ rhs_kernel(const double* __restrict__ X, const double* __restrict__ Y,
         double v[8];
         if (ev) {
             load_plane(X, Y, Z, n1, n2, ei, ej, ek + 1, x, 1);
-            const i64 e = ((i64)ek * ny + ej) * nx + ei;
-            const double u = __ldg(u0 + e), w1 = __ldg(u0 + E + e), w2 = __ldg(u0 + 2 * E + e);
+            const i64 e = ((i64)ek * u0.n2a + ej + u0.jofs) * nx + ei;
+            const double u = __ldg(u0.p + e), w1 = __ldg(u0.p + EC + e), w2 = __ldg(u0.p + 2 * EC + e);
             double Ji[3][3];
             const double det = centre_jacobian(x, Ji);
             double g[3];
@@ -272,35 +275,39 @@ rhs_kernel(const double* __restrict__ X, const double* __restrict__ Y,
                     s += fe[a][te];
                     s2 += fe[a + 4][te];
                 }
-            f[((i64)ek * n2 + nj) * n1 + ni] = ndir ? 0.0 : s;
+            fo[((i64)ek * f.n2a + nj + f.jofs) * n1 + ni] = ndir ? 0.0 : s;
             top = s2;
         }
         __syncthreads();
     }
-    if (nv) f[((i64)nz * n2 + nj) * n1 + ni] = 0.0;   // top plane is Dirichlet
+    if (nv) fo[((i64)nz * f.n2a + nj + f.jofs) * n1 + ni] = 0.0;   // top plane is Dirichlet
 }
 
 // ------------------------------------------------------------------ recovery
 // u_e = u0_e + c .* (Ji(0)^T g),  g_d = sum_a lambda_a s_ad / 8
+// Owned element rows: local rows [own0, own1) that are element rows of the grid.
 __global__ void __launch_bounds__(256)
 recover_kernel(const double* __restrict__ X, const double* __restrict__ Y,
-               const double* __restrict__ Z, int n1, int n2, int n3, double c0, double c1,
-               double c2, const double* __restrict__ lam, const double* __restrict__ u0,
-               double* __restrict__ u) {
+               const double* __restrict__ Z, LevDev L, double c0, double c1, double c2,
+               Nat lam, Nat u0, Nat u) {
+    const int n1 = L.n1, n2 = L.n2, n3 = L.n3;
     const int ei = blockIdx.x * blockDim.x + threadIdx.x;
-    const int ej = blockIdx.y;
-    const int nx = n1 - 1, ny = n2 - 1, nz = n3 - 1;
-    if (ei >= nx) return;
-    const i64 E = (i64)nx * ny * nz;
+    const int ej = L.own0 + (int)blockIdx.y;
+    const int nx = n1 - 1, nz = n3 - 1;
+    if (ei >= nx || ej >= L.own1 || ej + L.jg0 > L.n2g - 2) return;
+    const i64 EC = (i64)nz * u0.n2a * nx, EU = (i64)nz * u.n2a * nx;
+    double* uo = const_cast<double*>(u.p);
+    auto lat = [&](int k, int j, int i) {
+        return __ldg(lam.p + ((i64)k * lam.n2a + j + lam.jofs) * n1 + i);
+    };
     double x[8][3], l[8];
     load_plane(X, Y, Z, n1, n2, ei, ej, 0, x, 0);
 #pragma unroll
-    for (int q = 0; q < 4; q++) l[q] = __ldg(lam + (i64)(ej + (q >> 1)) * n1 + ei + (q & 1));
+    for (int q = 0; q < 4; q++) l[q] = lat(0, ej + (q >> 1), ei + (q & 1));
     for (int ek = 0; ek < nz; ek++) {
         load_plane(X, Y, Z, n1, n2, ei, ej, ek + 1, x, 1);
 #pragma unroll
-        for (int q = 0; q < 4; q++)
-            l[q + 4] = __ldg(lam + ((i64)(ek + 1) * n2 + ej + (q >> 1)) * n1 + ei + (q & 1));
+        for (int q = 0; q < 4; q++) l[q + 4] = lat(ek + 1, ej + (q >> 1), ei + (q & 1));
         double Ji[3][3];
         centre_jacobian(x, Ji);
         double g[3];
@@ -311,14 +318,15 @@ recover_kernel(const double* __restrict__ X, const double* __restrict__ Y,
             for (int a = 0; a < 8; a++) s = fma(l[a], sgn(a, d), s);
             g[d] = 0.125 * s;
         }
-        const i64 e = ((i64)ek * ny + ej) * nx + ei;
+        const i64 e = ((i64)ek * u0.n2a + ej + u0.jofs) * nx + ei;
+        const i64 eo = ((i64)ek * u.n2a + ej + u.jofs) * nx + ei;
         const double gx = Ji[0][0] * g[0] + Ji[1][0] * g[1] + Ji[2][0] * g[2];
         const double gy = Ji[0][1] * g[0] + Ji[1][1] * g[1] + Ji[2][1] * g[2];
         const double gz = Ji[0][2] * g[0] + Ji[1][2] * g[1] + Ji[2][2] * g[2];
-        const double a0 = __ldg(u0 + e), a1 = __ldg(u0 + E + e), a2 = __ldg(u0 + 2 * E + e);
-        u[e] = fma(c0, gx, a0);
-        u[E + e] = fma(c1, gy, a1);
-        u[2 * E + e] = fma(c2, gz, a2);
+        const double a0 = __ldg(u0.p + e), a1 = __ldg(u0.p + EC + e), a2 = __ldg(u0.p + 2 * EC + e);
+        uo[eo] = fma(c0, gx, a0);
+        uo[EU + eo] = fma(c1, gy, a1);
+        uo[2 * EU + eo] = fma(c2, gz, a2);
 #pragma unroll
         for (int q = 0; q < 4; q++) {
             x[q][0] = x[q + 4][0];
@@ -341,19 +349,19 @@ void launch_assemble(const double* X, const double* Y, const double* Z, int n1, 
     assemble_kernel<<<grid, NTH, smem, st>>>(X, Y, Z, n1, n2, n3, c[0], c[1], c[2], L, coef, bad);
 }
 
-void launch_rhs(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
-                const double* u0, double* f, cudaStream_t st) {
-    dim3 grid((n1 + TX - 2) / (TX - 1), (n2 + TY - 2) / (TY - 1));
+void launch_rhs(const double* X, const double* Y, const double* Z, const LevDev& L, Nat u0, Nat f,
+                cudaStream_t st) {
+    dim3 grid((L.n1 + TX - 2) / (TX - 1), (L.n2 + TY - 2) / (TY - 1));
     g_launches += 1;
-    rhs_kernel<<<grid, NTH, 0, st>>>(X, Y, Z, n1, n2, n3, u0, f);
+    rhs_kernel<<<grid, NTH, 0, st>>>(X, Y, Z, L, u0, f);
 }
 
-void launch_recover(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
-                    const double c[3], const double* lam, const double* u0, double* u,
-                    cudaStream_t st) {
-    dim3 grid((n1 - 1 + 127) / 128, n2 - 1);
+void launch_recover(const double* X, const double* Y, const double* Z, const LevDev& L,
+                    const double c[3], Nat lam, Nat u0, Nat u, cudaStream_t st) {
+    if (L.own1 <= L.own0) return;
+    dim3 grid((L.n1 - 1 + 127) / 128, L.own1 - L.own0);
     g_launches += 1;
-    recover_kernel<<<grid, 128, 0, st>>>(X, Y, Z, n1, n2, n3, c[0], c[1], c[2], lam, u0, u);
+    recover_kernel<<<grid, 128, 0, st>>>(X, Y, Z, L, c[0], c[1], c[2], lam, u0, u);
 }
 
 }  // namespace wd

@@ -77,8 +77,9 @@ gs_phase_kernel(LevDev L, const double* __restrict__ K, double* lam,
                 const double* __restrict__ f, int ci, int cj) {
     const int a = blockIdx.x * GS_BLK + threadIdx.x;
     const int i = 2 * a + ci;
-    const int j = 2 * blockIdx.y + cj;
-    if (i < 1 || i > L.n1 - 2 || j < 1 || j > L.n2 - 2) return;
+    // owned local rows whose global row has parity cj
+    const int j = L.own0 + ((cj - (L.own0 + L.jg0)) & 1) + 2 * (int)blockIdx.y;
+    if (i < 1 || i > L.n1 - 2 || !row_free(L, j)) return;
     i64 co[9];
     column_offsets(L, ci, co);
     const i64 own = loff(L, i, j, 0);
@@ -146,7 +147,7 @@ apply_kernel(LevDev L, const double* __restrict__ K, const double* __restrict__ 
     }
     const int i = 2 * a + ci;
     double acc = 0.0;
-    if (i >= 1 && i <= L.n1 - 2 && j >= 1 && j <= L.n2 - 2) {
+    if (i >= 1 && i <= L.n1 - 2 && row_free(L, j)) {
         i64 co[9];
         column_offsets(L, ci, co);
         const i64 own = loff(L, i, j, 0);
@@ -203,30 +204,29 @@ __global__ void __launch_bounds__(256) norm2_partial_kernel(const double* __rest
     if (threadIdx.x == 0) partial[blockIdx.x] = acc;
 }
 
-// natural [k][j][i] <-> internal i-split layout
-__global__ void nat2int_kernel(LevDev L, const double* __restrict__ src, double* __restrict__ dst,
-                               int zero_dir) {
+// natural [k][j][i] (ABI arrays, described by Nat) <-> internal i-split layout
+__global__ void nat2int_kernel(LevDev L, Nat src, double* __restrict__ dst, int zero_dir) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y, k = blockIdx.z;
     if (i >= L.n1) return;
-    double v = src[((i64)k * L.n2 + j) * L.n1 + i];
-    if (zero_dir && (i == 0 || i == L.n1 - 1 || j == 0 || j == L.n2 - 1 || k == L.n3 - 1))
-        v = 0.0;
+    double v = src.p[((i64)k * src.n2a + j + src.jofs) * L.n1 + i];
+    if (zero_dir && (i == 0 || i == L.n1 - 1 || row_dirichlet(L, j) || k == L.n3 - 1)) v = 0.0;
     dst[loff(L, i, j, k)] = v;
 }
 
-__global__ void int2nat_kernel(LevDev L, const double* __restrict__ src, double* __restrict__ dst) {
+// internal -> natural, owned rows only
+__global__ void int2nat_kernel(LevDev L, const double* __restrict__ src, Nat dst) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y, k = blockIdx.z;
-    if (i >= L.n1) return;
-    dst[((i64)k * L.n2 + j) * L.n1 + i] = src[loff(L, i, j, k)];
+    const int j = L.own0 + (int)blockIdx.y, k = blockIdx.z;
+    if (i >= L.n1 || j >= L.own1) return;
+    const_cast<double*>(dst.p)[((i64)k * dst.n2a + j + dst.jofs) * L.n1 + i] = src[loff(L, i, j, k)];
 }
 
 __global__ void zero_dirichlet_kernel(LevDev L, double* v) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y, k = blockIdx.z;
     if (i >= L.n1) return;
-    if (i == 0 || i == L.n1 - 1 || j == 0 || j == L.n2 - 1 || k == L.n3 - 1) v[loff(L, i, j, k)] = 0.0;
+    if (i == 0 || i == L.n1 - 1 || row_dirichlet(L, j) || k == L.n3 - 1) v[loff(L, i, j, k)] = 0.0;
 }
 
 // 1-D support of coarse index c along one direction: fine indices and weights
@@ -245,7 +245,7 @@ restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
                 double* __restrict__ fc) {
     const int I = blockIdx.x * 128 + threadIdx.x;
     const int J = blockIdx.y;
-    if (I < 1 || I > C.n1 - 2 || J < 1 || J > C.n2 - 2) return;
+    if (I < 1 || I > C.n1 - 2 || !row_free(C, J)) return;
     int tx[3], ty[3];
     double wx[3], wy[3];
     const int mx = support1d(M.pos[0], M.co[0], F.n1, I, tx, wx);
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(128)
 prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc, double* x) {
     const int i = blockIdx.x * 128 + threadIdx.x;
     const int j = blockIdx.y;
-    if (i < 1 || i > F.n1 - 2 || j < 1 || j > F.n2 - 2) return;
+    if (i < 1 || i > F.n1 - 2 || !row_free(F, j)) return;
     const int ix = M.lo[0][i], iy = M.lo[1][j];
     const int nx = M.co[0][i] ? 1 : 2, ny = M.co[1][j] ? 1 : 2;
     const double wx = nx == 1 ? 1.0 : 0.5, wy = ny == 1 ? 1.0 : 0.5;
@@ -302,7 +302,7 @@ galerkin_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ KF,
                 double* __restrict__ KC) {
     const int I = blockIdx.x * 128 + threadIdx.x;
     const int J = blockIdx.y, Kc = blockIdx.z;
-    if (I < 1 || I > C.n1 - 2 || J < 1 || J > C.n2 - 2 || Kc > C.n3 - 2) return;
+    if (I < 1 || I > C.n1 - 2 || !row_free(C, J) || Kc > C.n3 - 2) return;
     int pt[3][3];
     double pw[3][3];
     int pm[3];
@@ -402,13 +402,12 @@ dim3 node_grid(const LevDev& L) { return dim3((L.n1 + 127) / 128, L.n2, L.n3); }
 
 }  // namespace
 
-void launch_nat2int(const LevDev& L, const double* src, double* dst, bool zero_dirichlet,
-                    cudaStream_t st) {
+void launch_nat2int(const LevDev& L, Nat src, double* dst, bool zero_dirichlet, cudaStream_t st) {
     g_launches += 1;
     nat2int_kernel<<<node_grid(L), 128, 0, st>>>(L, src, dst, zero_dirichlet ? 1 : 0);
 }
 
-void launch_int2nat(const LevDev& L, const double* src, double* dst, cudaStream_t st) {
+void launch_int2nat(const LevDev& L, const double* src, Nat dst, cudaStream_t st) {
     g_launches += 1;
     int2nat_kernel<<<node_grid(L), 128, 0, st>>>(L, src, dst);
 }
@@ -418,14 +417,31 @@ void launch_zero_dirichlet(const LevDev& L, double* v, cudaStream_t st) {
     zero_dirichlet_kernel<<<node_grid(L), 128, 0, st>>>(L, v);
 }
 
+// colour phase c of the smoother: (i mod 2, j mod 2) = (0,0),(1,0),(0,1),(1,1) (reading C7)
+void launch_gs_phase(const LevDev& L, const double* coef, double* lam, const double* f, int c,
+                     cudaStream_t st) {
+    static const int colour[4][2] = {{0, 0}, {1, 0}, {0, 1}, {1, 1}};
+    const int half = (L.n1 + 1) / 2;
+    dim3 grid((half + GS_BLK - 1) / GS_BLK, (L.own1 - L.own0 + 2) / 2);
+    g_launches += 1;
+    gs_phase_kernel<<<grid, GS_BLK, 0, st>>>(L, coef, lam, f, colour[c][0], colour[c][1]);
+}
+
 void launch_gs_sweep(const LevDev& L, const double* coef, double* lam, const double* f,
                      cudaStream_t st) {
-    static const int colour[4][2] = {{0, 0}, {1, 0}, {0, 1}, {1, 1}};   // (i mod 2, j mod 2)
-    const int half = (L.n1 + 1) / 2;
-    dim3 grid((half + GS_BLK - 1) / GS_BLK, (L.n2 + 1) / 2);
-    g_launches += 4;
-    for (int c = 0; c < 4; c++)
-        gs_phase_kernel<<<grid, GS_BLK, 0, st>>>(L, coef, lam, f, colour[c][0], colour[c][1]);
+    for (int c = 0; c < 4; c++) launch_gs_phase(L, coef, lam, f, c, st);
+}
+
+__global__ void sum_ordered_kernel(const double* __restrict__ v, int n, double* out) {
+    double s = 0.0;
+    for (int t = 0; t < n; t++) s += v[t];
+    *out = s;
+}
+
+// out = v[0] + v[1] + ... + v[n-1] in this order (rank-ordered partial sums)
+void launch_sum_ordered(const double* v, int n, double* out, cudaStream_t st) {
+    g_launches += 1;
+    sum_ordered_kernel<<<1, 1, 0, st>>>(v, n, out);
 }
 
 int launch_apply(const LevDev& L, const double* coef, const double* x, const double* f, double* y,

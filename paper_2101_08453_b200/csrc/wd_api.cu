@@ -1,13 +1,28 @@
-// wd_api.cu -- the C ABI (include/wd.h): context, host planner, V-cycle
-// driver and solve loop on top of the sm_100a kernels.
+// wd_api.cu -- the C ABI (include/wd.h): context, host planner, slab
+// decomposition and transport, V-cycle driver and solve loop on top of the
+// sm_100a kernels.
 //
 // Host-side work is control only: argument checks, the coarsening plan
-// (PAPER.md P:192-202 applied to a handful of spacings), launch sequencing,
-// CUDA-graph capture of the V-cycle and the convergence test on one scalar
-// per cycle.  Every array operation of the path runs in the kernels of
-// k_fe.cu, k_mg.cu and k_coarse.cu.
+// (PAPER.md P:192-202 applied to a handful of spacings), the row partition,
+// launch sequencing, halo exchanges, CUDA-graph capture of the V-cycle and the
+// convergence test on one scalar per cycle.  Every array operation of the path
+// runs in the kernels of k_fe.cu, k_mg.cu, k_apply_tma.cu and k_coarse.cu.
+//
+// Decomposition (requirement (1) of P:39-40): the grid is split
+// into slabs of node rows j.  A context holds one "part" per slab it drives:
+//   * single GPU:      1 part, the whole grid, no transport;
+//   * NCCL (one process per GPU): 1 part (this rank's slab), halo rows are
+//     exchanged with ncclSend/ncclRecv, coarse levels gathered by ncclBroadcast;
+//   * virtual ranks:   R parts of one grid on one GPU, the same exchanges as
+//     device-to-device copies (tests the decomposition logic bit for bit).
+// Every part keeps 2 halo rows on each side.  Levels below the gather level
+// are distributed; from the gather level on every part holds the whole
+// (small) level and computes it redundantly (identical results).
 #include "../../include/wd.h"
 #include "wd_internal.cuh"
+
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -48,75 +63,148 @@ int fail(int code, const char* fmt, ...) {
                         __FILE__, __LINE__);                                                   \
     } while (0)
 
+#define RC(x)                \
+    do {                     \
+        int rc_ = (x);       \
+        if (rc_) return rc_; \
+    } while (0)
+
 constexpr int MAXLEV = 32;
 constexpr int MAXNZ = 512;
+constexpr int HALO = 2;          // halo rows of every slab, each side
+constexpr int MIN_OWNED = 4;     // fewer owned rows on any rank -> gather
 
-LevDev make_level(int n1, int n2, int n3) {
+LevDev make_level(int n1, int n2, int n3, int jg0, int n2g, int own0, int own1) {
     LevDev L;
     L.n1 = n1;
     L.n2 = n2;
     L.n3 = n3;
     int half = (n1 + 1) / 2;
-    L.H = std::max((half + 15) / 16 * 16, 48);   // >= the TMA box width (34)
+    L.H = std::max((half + 15) / 16 * 16, 48);   // >= the TMA box width (36)
     L.P = 2 * L.H;
     L.sk = L.P;
     L.sj = (i64)n3 * L.P;
     L.NT = (i64)n2 * L.sj;
+    L.jg0 = jg0;
+    L.n2g = n2g;
+    L.own0 = own0;
+    L.own1 = own1;
     return L;
 }
 
-i64 level_free(const LevDev& L) { return (i64)(L.n1 - 2) * (L.n2 - 2) * (L.n3 - 1); }
+i64 free_count(int n1, int n2, int n3) { return (i64)(n1 - 2) * (n2 - 2) * (n3 - 1); }
 
 struct Level {
     LevDev L;
+    bool dist = false;        // distributed (slab) level; else replicated / single
+    int cown0 = 0, cown1 = 0; // rows this part computes when restricting / forming K_c into
+                              // this level (= owned rows; a slice of the gather level)
     double* coef = nullptr;   // 14 * NT
     double* lam = nullptr;
     double* f = nullptr;
     double* r = nullptr;
-    double* raw[4] = {nullptr, nullptr, nullptr, nullptr};   // allocations (with front guard)
+    double* raw[4] = {nullptr, nullptr, nullptr, nullptr};
     // transition to level + 1
     int hflag = 0;
     int nkept = 0;
     int kept[MAXNZ];
-    int* dmap = nullptr;      // device: lo/co/pos for 3 directions
+    int* dmap = nullptr;      // device: lo/co/pos for 3 directions (y local to the part)
     MapDev M;
-    // TMA tensor maps (CUtensorMap, 128 B each): coefficient slots 0-4 and 5-13,
-    // x = lam (halo box) and f (tile box) of this level
     alignas(64) unsigned char tmA[128], tmB[128], tmX[128], tmF[128];
 };
 
-// residual r = f - K lam (f_on) or r = K lam on level `lv`; optional per-CTA partials
-int apply_level(Level& lv, bool f_on, double* partial, cudaStream_t st) {
-    if (g_apply_variant >= 0)
-        return launch_apply_tma(lv.L, lv.tmA, lv.tmB, lv.tmX, f_on ? lv.tmF : nullptr, lv.r,
-                                partial, st);
-    return launch_apply(lv.L, lv.coef, lv.lam, f_on ? lv.f : nullptr, lv.r, partial, st);
-}
-
-}  // namespace
-
-struct wd_ctx {
-    int n1, n2, n3;
-    double a[3], c[3];
-    wd_options opt;
-    double *X = nullptr, *Y = nullptr, *Z = nullptr;
-    int nlev = 0;
-    Level lev[MAXLEV];
-    int coarse_direct = 0;
-    int nf = 0;
+struct Part {
+    int rank = 0;
+    int jlo = 0, jhi = 0;     // level-0 local rows = global rows [jlo, jhi)
+    int own0g = 0, own1g = 0; // owned global rows at level 0
+    double *X = nullptr, *Y = nullptr, *Z = nullptr;   // local coordinates (natural layout)
     double* Ainv = nullptr;
     double* Dinv = nullptr;
     double* partial = nullptr;
     int npartial = 0;
-    double* dscal = nullptr;    // device scalars
-    double* hscal = nullptr;    // pinned host scalars
-    cudaStream_t cap = nullptr; // capture stream
+    Level lev[MAXLEV];
+};
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct Nccl {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Bcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    const char* (*ErrStr)(ncclResult_t);
+};
+
+Nccl& nccl() {
+    static Nccl n;
+    static bool tried = false;
+    if (tried) return n;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return n;
+#define SYM(f, name) n.f = reinterpret_cast<decltype(n.f)>(dlsym(h, name))
+    SYM(GetUniqueId, "ncclGetUniqueId");
+    SYM(CommInitRank, "ncclCommInitRank");
+    SYM(CommDestroy, "ncclCommDestroy");
+    SYM(Send, "ncclSend");
+    SYM(Recv, "ncclRecv");
+    SYM(Bcast, "ncclBroadcast");
+    SYM(AllGather, "ncclAllGather");
+    SYM(AllReduce, "ncclAllReduce");
+    SYM(GroupStart, "ncclGroupStart");
+    SYM(GroupEnd, "ncclGroupEnd");
+    SYM(ErrStr, "ncclGetErrorString");
+#undef SYM
+    n.ok = n.GetUniqueId && n.CommInitRank && n.Send && n.Recv && n.Bcast && n.AllGather &&
+           n.AllReduce && n.GroupStart && n.GroupEnd;
+    return n;
+}
+
+#define NK(call)                                                                               \
+    do {                                                                                       \
+        ncclResult_t r_ = (call);                                                              \
+        if (r_ != ncclSuccess)                                                                 \
+            return fail(WD_E_NCCL, "%s failed: %s", #call,                                     \
+                        nccl().ErrStr ? nccl().ErrStr(r_) : "nccl error");                     \
+    } while (0)
+
+enum { MODE_SINGLE = 0, MODE_NCCL = 1, MODE_VIRTUAL = 2 };
+
+}  // namespace
+
+struct wd_ctx {
+    int n1, n2, n3;            // global node dims
+    double a[3], c[3];
+    wd_options opt;
+    int mode = MODE_SINGLE;
+    int nranks = 1, rank = 0;  // this process's rank (NCCL mode)
+    ncclComm_t comm = nullptr;
+    std::vector<int> own0g, own1g;   // owned level-0 rows of every rank
+    // per level, per rank: global rows the rank owns (distributed levels) or
+    // contributes before the gather (the gather level)
+    std::vector<std::vector<std::pair<int, int>>> rrows;
+    std::vector<Part> parts;
+    int nlev = 0;
+    int gather = MAXLEV;       // first replicated level (multi-rank), MAXLEV if none
+    int levdims[MAXLEV][3];    // global node dims per level
+    int coarse_direct = 0;
+    int nf = 0;
+    double* dscal = nullptr;   // device scalars
+    double* hscal = nullptr;   // pinned host scalars
+    cudaStream_t cap = nullptr;
     cudaGraphExec_t vgraph = nullptr;
     long long bytes = 0;
     std::vector<std::pair<void*, size_t>> pool;   // staging buffers for host pointers
     std::vector<int> pool_busy;
-    long long graph_kernels = 0;                  // kernel nodes of the V-cycle graph
-    // profiling (opt.profile): events around level-0 sweeps, the V-cycle, the residual
+    long long graph_kernels = 0;
     cudaEvent_t ev_gs[32] = {};
     cudaEvent_t ev_cyc[2] = {};
     cudaEvent_t ev_res[2] = {};
@@ -130,9 +218,7 @@ int g_apply_variant = 1;
 
 namespace {
 
-// Device allocations come from the device's default stream-ordered memory pool
-// with an unlimited release threshold, so a context built after another one
-// was destroyed reuses the retained memory instead of remapping it.
+// ------------------------------------------------------------------ memory
 void ensure_pool() {
     static bool done[64] = {};
     int dev = 0;
@@ -147,6 +233,9 @@ void ensure_pool() {
     done[dev] = true;
 }
 
+// Device allocations come from the stream-ordered pool of the device with an
+// unlimited release threshold: a context built after another one was destroyed
+// reuses the retained memory instead of remapping it.
 int dalloc(wd_ctx* ctx, void** p, size_t bytes) {
     ensure_pool();
     const size_t b = bytes > 0 ? bytes : 8;
@@ -200,8 +289,7 @@ int stage_acquire(wd_ctx* ctx, Stage& s, size_t bytes) {
                 return WD_OK;
             }
         void* p;
-        int rc = dalloc(nullptr, &p, bytes);
-        if (rc) return rc;
+        RC(dalloc(nullptr, &p, bytes));
         ctx->pool.push_back({p, bytes});
         ctx->pool_busy.push_back(1);
         s.slot = (int)ctx->pool.size() - 1;
@@ -221,8 +309,7 @@ int stage_in(wd_ctx* ctx, Stage& s, const double* p, size_t n, cudaStream_t st) 
         return WD_OK;
     }
     s.staged = true;
-    int rc = stage_acquire(ctx, s, s.bytes);
-    if (rc) return rc;
+    RC(stage_acquire(ctx, s, s.bytes));
     CK(cudaMemcpyAsync(s.d, p, s.bytes, cudaMemcpyHostToDevice, st));
     return WD_OK;
 }
@@ -240,7 +327,7 @@ int stage_out(wd_ctx* ctx, Stage& s, double* p, size_t n) {
     return stage_acquire(ctx, s, s.bytes);
 }
 
-// finish: copy staged outputs back, synchronise if anything was staged, release
+// copy staged outputs back, synchronise if anything was staged, release
 int stage_finish(cudaStream_t st, std::initializer_list<Stage*> list) {
     bool any = false;
     for (Stage* s : list) {
@@ -315,70 +402,223 @@ int horiz_kept(int n, int* pos) {
     return m;
 }
 
-int alloc_level(wd_ctx* ctx, Level& lv, int n1, int n2, int n3) {
-    lv.L = make_level(n1, n2, n3);
+// rows [a, b) of a fine level -> coarse rows J with pos[J] in [a, b)
+void coarse_range(const std::vector<int>& pos, int a, int b, int& c0, int& c1) {
+    c0 = (int)(std::lower_bound(pos.begin(), pos.end(), a) - pos.begin());
+    c1 = (int)(std::lower_bound(pos.begin(), pos.end(), b) - pos.begin());
+}
+
+int alloc_level(wd_ctx* ctx, Level& lv) {
     const size_t nt = (size_t)lv.L.NT;
-    int rc;
-    const size_t g = 0;   // front guard (doubles) before each array
     double** arr[4] = {&lv.coef, &lv.lam, &lv.f, &lv.r};
     const size_t len[4] = {14 * nt, nt, nt, nt};
     for (int t = 0; t < 4; t++) {
-        if ((rc = dalloc(ctx, (void**)&lv.raw[t], sizeof(double) * (len[t] + g)))) return rc;
-        *arr[t] = lv.raw[t] + g;
+        RC(dalloc(ctx, (void**)&lv.raw[t], sizeof(double) * len[t]));
+        *arr[t] = lv.raw[t];
     }
     if (make_coef_maps(lv.L, lv.coef, lv.tmA, lv.tmB) || make_vec_map(lv.L, lv.lam, lv.tmX, true) ||
         make_vec_map(lv.L, lv.f, lv.tmF, false))
-        return fail(WD_E_CUDA, "cuTensorMapEncodeTiled failed for level dims (%d,%d,%d)", n1, n2, n3);
+        return fail(WD_E_CUDA, "cuTensorMapEncodeTiled failed for level dims (%d,%d,%d)", lv.L.n1,
+                    lv.L.n2, lv.L.n3);
+    return WD_OK;
+}
+
+// residual r = f - K lam (f_on) or r = K lam on level `lv`; optional per-CTA partials
+int apply_level(Level& lv, bool f_on, double* partial, cudaStream_t st) {
+    if (g_apply_variant >= 0)
+        return launch_apply_tma(lv.L, lv.tmA, lv.tmB, lv.tmX, f_on ? lv.tmF : nullptr, lv.r,
+                                partial, st);
+    return launch_apply(lv.L, lv.coef, lv.lam, f_on ? lv.f : nullptr, lv.r, partial, st);
+}
+
+// level with the compute rows [cown0, cown1) (restriction / Galerkin target)
+LevDev target(const Level& lv) {
+    LevDev L = lv.L;
+    L.own0 = lv.cown0;
+    L.own1 = lv.cown1;
+    return L;
+}
+
+// ------------------------------------------------------------------ transport
+enum { ARR_LAM = 0, ARR_R = 1, ARR_COEF = 2, ARR_F = 3 };
+
+double* arr_of(Level& lv, int which) {
+    return which == ARR_LAM ? lv.lam : which == ARR_R ? lv.r : which == ARR_F ? lv.f : lv.coef;
+}
+
+// Halo exchange of w rows each side on a distributed level: a part's first w
+// owned rows go to the upper halo of the rank below, its last w owned rows to
+// the lower halo of the rank above (all levels of a row are contiguous).
+int exchange(wd_ctx* ctx, int l, int which, int w, cudaStream_t st) {
+    if (ctx->mode == MODE_SINGLE || !ctx->parts[0].lev[l].dist) return WD_OK;
+    const int np = which == ARR_COEF ? 14 : 1;
+    if (ctx->mode == MODE_VIRTUAL) {
+        const int R = (int)ctx->parts.size();
+        for (int p = 0; p < R; p++) {
+            Level& me = ctx->parts[p].lev[l];
+            const LevDev& L = me.L;
+            for (int pl = 0; pl < np; pl++) {
+                const double* src = arr_of(me, which) + (i64)pl * L.NT;
+                if (p > 0) {
+                    Level& dn = ctx->parts[p - 1].lev[l];
+                    double* dst = arr_of(dn, which) + (i64)pl * dn.L.NT;
+                    CK(cudaMemcpyAsync(dst + (i64)dn.L.own1 * dn.L.sj, src + (i64)L.own0 * L.sj,
+                                       sizeof(double) * w * L.sj, cudaMemcpyDeviceToDevice, st));
+                }
+                if (p < R - 1) {
+                    Level& up = ctx->parts[p + 1].lev[l];
+                    double* dst = arr_of(up, which) + (i64)pl * up.L.NT;
+                    CK(cudaMemcpyAsync(dst + (i64)(up.L.own0 - w) * up.L.sj,
+                                       src + (i64)(L.own1 - w) * L.sj, sizeof(double) * w * L.sj,
+                                       cudaMemcpyDeviceToDevice, st));
+                }
+            }
+        }
+        return WD_OK;
+    }
+    // NCCL: one process per GPU, this rank's single part
+    Nccl& N = nccl();
+    Level& me = ctx->parts[0].lev[l];
+    const LevDev& L = me.L;
+    const size_t cnt = (size_t)w * L.sj;
+    NK(N.GroupStart());
+    for (int pl = 0; pl < np; pl++) {
+        double* a = arr_of(me, which) + (i64)pl * L.NT;
+        if (ctx->rank > 0) {
+            NK(N.Send(a + (i64)L.own0 * L.sj, cnt, ncclDouble, ctx->rank - 1, ctx->comm, st));
+            NK(N.Recv(a + (i64)(L.own0 - w) * L.sj, cnt, ncclDouble, ctx->rank - 1, ctx->comm, st));
+        }
+        if (ctx->rank < ctx->nranks - 1) {
+            NK(N.Send(a + (i64)(L.own1 - w) * L.sj, cnt, ncclDouble, ctx->rank + 1, ctx->comm, st));
+            NK(N.Recv(a + (i64)L.own1 * L.sj, cnt, ncclDouble, ctx->rank + 1, ctx->comm, st));
+        }
+    }
+    NK(N.GroupEnd());
+    return WD_OK;
+}
+
+// Gather level: every rank computed the rows [cown0, cown1) of the (full)
+// level; give every rank all rows.
+int gather_rows(wd_ctx* ctx, int l, int which, cudaStream_t st) {
+    if (ctx->mode == MODE_SINGLE) return WD_OK;
+    const int np = which == ARR_COEF ? 14 : 1;
+    if (ctx->mode == MODE_VIRTUAL) {
+        const int R = (int)ctx->parts.size();
+        for (int p = 0; p < R; p++) {
+            Level& src = ctx->parts[p].lev[l];
+            const size_t n = (size_t)(src.cown1 - src.cown0) * src.L.sj;
+            if (!n) continue;
+            for (int q = 0; q < R; q++) {
+                if (q == p) continue;
+                Level& dst = ctx->parts[q].lev[l];
+                for (int pl = 0; pl < np; pl++)
+                    CK(cudaMemcpyAsync(arr_of(dst, which) + (i64)pl * dst.L.NT + (i64)src.cown0 * src.L.sj,
+                                       arr_of(src, which) + (i64)pl * src.L.NT + (i64)src.cown0 * src.L.sj,
+                                       sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        return WD_OK;
+    }
+    Nccl& N = nccl();
+    Level& me = ctx->parts[0].lev[l];
+    NK(N.GroupStart());
+    for (int r = 0; r < ctx->nranks; r++) {
+        const int a = ctx->rrows[l][r].first, b = ctx->rrows[l][r].second;   // rank r's rows
+        const size_t n = (size_t)(b - a) * me.L.sj;
+        if (!n) continue;
+        for (int pl = 0; pl < np; pl++) {
+            double* buf = arr_of(me, which) + (i64)pl * me.L.NT + (i64)a * me.L.sj;
+            NK(N.Bcast(buf, buf, n, ncclDouble, r, ctx->comm, st));
+        }
+    }
+    NK(N.GroupEnd());
+    return WD_OK;
+}
+
+// sum of one device scalar per rank, in rank order (identical on every rank
+// and in every mode): in = per-part scalars (virtual) or this rank's scalar
+int sum_ranks(wd_ctx* ctx, const double* in, double* out, cudaStream_t st) {
+    if (ctx->mode == MODE_SINGLE) {
+        if (in != out) CK(cudaMemcpyAsync(out, in, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        return WD_OK;
+    }
+    double* tmp = ctx->dscal + 256;   // nranks values
+    if (ctx->mode == MODE_VIRTUAL) {
+        CK(cudaMemcpyAsync(tmp, in, sizeof(double) * ctx->parts.size(), cudaMemcpyDeviceToDevice, st));
+    } else {
+        NK(nccl().AllGather(in, tmp, 1, ncclDouble, ctx->comm, st));
+    }
+    launch_sum_ordered(tmp, ctx->nranks, out, st);
+    CKL();
     return WD_OK;
 }
 
 // ------------------------------------------------------------------ V-cycle
+int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st);
+
 int coarse_solve(wd_ctx* ctx, cudaStream_t st) {
-    Level& lc = ctx->lev[ctx->nlev - 1];
+    const int l = ctx->nlev - 1;
     if (ctx->coarse_direct) {
-        if (ctx->nf > 0) launch_coarse_gemv(lc.L, ctx->Ainv, ctx->nf, lc.f, lc.lam, st);
-    } else {
-        CK(cudaMemsetAsync(lc.lam, 0, sizeof(double) * lc.L.NT, st));
-        for (int s = 0; s < ctx->opt.coarse_iters; s++) launch_gs_sweep(lc.L, lc.coef, lc.lam, lc.f, st);
+        for (Part& P : ctx->parts) {
+            Level& lc = P.lev[l];
+            if (ctx->nf > 0) launch_coarse_gemv(lc.L, P.Ainv, ctx->nf, lc.f, lc.lam, st);
+        }
+    } else {   // reading C8: GS sweeps from 0 (with halo exchanges on a slab level)
+        for (Part& P : ctx->parts) CK(cudaMemsetAsync(P.lev[l].lam, 0, sizeof(double) * P.lev[l].L.NT, st));
+        for (int s = 0; s < ctx->opt.coarse_iters; s++) RC(smooth(ctx, l, false, 0, st));
     }
     CKL();
+    return WD_OK;
+}
+
+// one smoothing sweep on level l: 4 colour phases; on slabs the boundary rows
+// are exchanged after phase 1 (even rows final) and phase 3 (odd rows final)
+int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st) {
+    if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns], st, cudaEventRecordExternal));
+    for (int c = 0; c < 4; c++) {
+        for (Part& P : ctx->parts) {
+            Level& F = P.lev[l];
+            launch_gs_phase(F.L, F.coef, F.lam, F.f, c, st);
+        }
+        if (c == 1 || c == 3) RC(exchange(ctx, l, ARR_LAM, 1, st));
+    }
+    if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns + 1], st, cudaEventRecordExternal));
     return WD_OK;
 }
 
 int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st) {
     if (l == ctx->nlev - 1) return coarse_solve(ctx, st);
-    Level& F = ctx->lev[l];
-    Level& C = ctx->lev[l + 1];
-    const bool prof = ctx->opt.profile && l == 0;
+    const bool prof = ctx->opt.profile && l == 0 && ctx->parts.size() == 1;
     int ns = 0;
-    for (int s = 0; s < ctx->opt.pre_smooth; s++, ns++) {
-        if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns], st, cudaEventRecordExternal));
-        launch_gs_sweep(F.L, F.coef, F.lam, F.f, st);
-        if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns + 1], st, cudaEventRecordExternal));
+    for (int s = 0; s < ctx->opt.pre_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
+    for (Part& P : ctx->parts) apply_level(P.lev[l], true, nullptr, st);
+    RC(exchange(ctx, l, ARR_R, 1, st));
+    for (Part& P : ctx->parts) {
+        Level& F = P.lev[l];
+        Level& C = P.lev[l + 1];
+        launch_restrict(F.L, target(C), F.M, F.r, C.f, st);
     }
-    apply_level(F, true, nullptr, st);
-    launch_restrict(F.L, C.L, F.M, F.r, C.f, st);
-    CK(cudaMemsetAsync(C.lam, 0, sizeof(double) * C.L.NT, st));
+    if (l + 1 == ctx->gather) RC(gather_rows(ctx, l + 1, ARR_F, st));
+    for (Part& P : ctx->parts) CK(cudaMemsetAsync(P.lev[l + 1].lam, 0, sizeof(double) * P.lev[l + 1].L.NT, st));
     CKL();
-    int rc = vcycle_level(ctx, l + 1, st);
-    if (rc) return rc;
-    launch_prolong(F.L, C.L, F.M, C.lam, F.lam, st);
-    for (int s = 0; s < ctx->opt.post_smooth; s++, ns++) {
-        if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns], st, cudaEventRecordExternal));
-        launch_gs_sweep(F.L, F.coef, F.lam, F.f, st);
-        if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns + 1], st, cudaEventRecordExternal));
+    RC(vcycle_level(ctx, l + 1, st));
+    for (Part& P : ctx->parts) {
+        Level& F = P.lev[l];
+        Level& C = P.lev[l + 1];
+        launch_prolong(F.L, C.L, F.M, C.lam, F.lam, st);
     }
+    RC(exchange(ctx, l, ARR_LAM, 1, st));
+    for (int s = 0; s < ctx->opt.post_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
     CKL();
     return WD_OK;
 }
 
-// after a synchronisation: add the elapsed times of the last V-cycle / residual
 void profile_accumulate(wd_ctx* ctx, bool cycle, bool resid) {
     if (!ctx->opt.profile) return;
     float ms;
     if (cycle) {
         const int ns = std::min(ctx->opt.pre_smooth + ctx->opt.post_smooth, 16);
-        if (ctx->nlev > 1)
+        if (ctx->nlev > 1 && ctx->parts.size() == 1)
             for (int s = 0; s < ns; s++)
                 if (cudaEventElapsedTime(&ms, ctx->ev_gs[2 * s], ctx->ev_gs[2 * s + 1]) == cudaSuccess) {
                     ctx->prof[0] += ms;
@@ -396,12 +636,10 @@ void profile_accumulate(wd_ctx* ctx, bool cycle, bool resid) {
     cudaGetLastError();
 }
 
-// one V-cycle on the internal level-0 vectors, optionally through a CUDA graph
 int run_vcycle(wd_ctx* ctx, cudaStream_t st) {
     if (ctx->opt.profile) CK(cudaEventRecord(ctx->ev_cyc[0], st));
     if (!ctx->opt.use_graph) {
-        int rc = vcycle_level(ctx, 0, st);
-        if (rc) return rc;
+        RC(vcycle_level(ctx, 0, st));
     } else {
         if (!ctx->vgraph) {
             const long long before = g_launches.load();
@@ -424,21 +662,37 @@ int run_vcycle(wd_ctx* ctx, cudaStream_t st) {
     return WD_OK;
 }
 
-// ||f - K lam||^2 of level 0 into dscal[slot] (device), stream-ordered
+// ||f - K lam||^2 over free nodes of level 0, all ranks, into dscal[slot]
 int residual_sq(wd_ctx* ctx, int slot, cudaStream_t st) {
-    Level& F = ctx->lev[0];
     if (ctx->opt.profile) CK(cudaEventRecord(ctx->ev_res[0], st));
-    int nb = apply_level(F, true, ctx->partial, st);
-    launch_reduce_sum(ctx->partial, nb, ctx->dscal + slot, st);
+    double* per = ctx->dscal + 128;   // per-part sums
+    for (size_t p = 0; p < ctx->parts.size(); p++) {
+        Part& P = ctx->parts[p];
+        int nb = apply_level(P.lev[0], true, P.partial, st);
+        launch_reduce_sum(P.partial, nb, per + p, st);
+    }
+    RC(sum_ranks(ctx, per, ctx->dscal + slot, st));
     if (ctx->opt.profile) CK(cudaEventRecord(ctx->ev_res[1], st));
     CKL();
     return WD_OK;
 }
 
-int norm_sq(wd_ctx* ctx, const LevDev& L, const double* v, int slot, cudaStream_t st) {
-    int nb;
-    launch_norm2_partial(L, v, ctx->partial, &nb, st);
-    launch_reduce_sum(ctx->partial, nb, ctx->dscal + slot, st);
+// sum of squares of the owned rows of an internal level-0 vector (all ranks)
+int norm_sq(wd_ctx* ctx, int which, int slot, cudaStream_t st) {
+    double* per = ctx->dscal + 128;
+    for (size_t p = 0; p < ctx->parts.size(); p++) {
+        Part& P = ctx->parts[p];
+        Level& lv = P.lev[0];
+        LevDev L = lv.L;
+        // owned rows only: view the owned block as a flat array
+        const double* v = arr_of(lv, which) + (i64)L.own0 * L.sj;
+        LevDev Lv = L;
+        Lv.NT = (i64)(L.own1 - L.own0) * L.sj;
+        int nb;
+        launch_norm2_partial(Lv, v, P.partial, &nb, st);
+        launch_reduce_sum(P.partial, nb, per + p, st);
+    }
+    RC(sum_ranks(ctx, per, ctx->dscal + slot, st));
     CKL();
     return WD_OK;
 }
@@ -455,7 +709,50 @@ int check_level(const wd_ctx* ctx, int level) {
     return WD_OK;
 }
 
+int check_single(const wd_ctx* ctx) {
+    if (ctx->mode != MODE_SINGLE) return fail(WD_E_INVAL, "inspection calls need a single-GPU context");
+    return WD_OK;
+}
+
 size_t nodes_of(const LevDev& L) { return (size_t)L.n1 * L.n2 * L.n3; }
+
+// ABI node / element arrays of part P: virtual ranks index the global array,
+// a NCCL rank its slab (rows jlo .. jhi-1), a single GPU the whole grid
+Nat nat_nodes(const wd_ctx* ctx, const Part& P, const double* p) {
+    Nat a;
+    a.p = p;
+    if (ctx->mode == MODE_VIRTUAL) { a.n2a = ctx->n2; a.jofs = P.jlo; }
+    else { a.n2a = P.jhi - P.jlo; a.jofs = 0; }
+    return a;
+}
+Nat nat_elems(const wd_ctx* ctx, const Part& P, const double* p) {
+    Nat a;
+    a.p = p;
+    if (ctx->mode == MODE_VIRTUAL) { a.n2a = ctx->n2 - 1; a.jofs = P.jlo; }
+    else { a.n2a = P.jhi - P.jlo - 1; a.jofs = 0; }
+    return a;
+}
+// element count / node count of the ABI arrays this context expects
+size_t abi_nodes(const wd_ctx* ctx) {
+    const Part& P = ctx->parts[0];
+    const int rows = ctx->mode == MODE_NCCL ? P.jhi - P.jlo : ctx->n2;
+    return (size_t)ctx->n1 * rows * ctx->n3;
+}
+size_t abi_elems(const wd_ctx* ctx) {
+    const Part& P = ctx->parts[0];
+    const int rows = ctx->mode == MODE_NCCL ? P.jhi - P.jlo : ctx->n2;
+    return (size_t)3 * (ctx->n1 - 1) * (rows - 1) * (ctx->n3 - 1);
+}
+
+// internal level-0 vector of every part -> ABI array (owned rows; a NCCL rank
+// also writes its halo rows, which are current after a V-cycle)
+void out_nodes(wd_ctx* ctx, const double* dst, cudaStream_t st) {
+    for (Part& P : ctx->parts) {
+        LevDev L = P.lev[0].L;
+        if (ctx->mode == MODE_NCCL) { L.own0 = 0; L.own1 = L.n2; }
+        launch_int2nat(L, P.lev[0].lam, nat_nodes(ctx, P, dst), st);
+    }
+}
 
 }  // namespace
 
@@ -470,6 +767,7 @@ void wd_default_options(wd_options* o) {
     o->coarse_iters = 50;
     o->coarsen_rule = WD_RULE_COUPLING_CUR;
     o->use_graph = 1;
+    o->gather_below_nodes = 2000000;
     o->rank = 0;
     o->nranks = 1;
 }
@@ -485,29 +783,55 @@ void wd_destroy(wd_ctx* ctx) {
     for (auto e : ctx->ev_gs) if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_cyc) if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_res) if (e) cudaEventDestroy(e);
-    for (int l = 0; l < ctx->nlev; l++) {
-        Level& lv = ctx->lev[l];
-        for (double* p : lv.raw) dfree(p);
-        dfree(lv.dmap);
+    for (Part& P : ctx->parts) {
+        for (int l = 0; l < ctx->nlev; l++) {
+            for (double* p : P.lev[l].raw) dfree(p);
+            dfree(P.lev[l].dmap);
+        }
+        dfree(P.X);
+        dfree(P.Y);
+        dfree(P.Z);
+        dfree(P.Ainv);
+        dfree(P.Dinv);
+        dfree(P.partial);
     }
-    dfree(ctx->X);
-    dfree(ctx->Y);
-    dfree(ctx->Z);
-    dfree(ctx->Ainv);
-    dfree(ctx->Dinv);
-    dfree(ctx->partial);
     dfree(ctx->dscal);
     if (ctx->hscal) cudaFreeHost(ctx->hscal);
     for (auto& p : ctx->pool) dfree(p.first);
+    if (ctx->comm && nccl().CommDestroy) nccl().CommDestroy(ctx->comm);
     delete ctx;
 }
 
 long long wd_device_bytes(const wd_ctx* ctx) { return ctx ? ctx->bytes : 0; }
 
+int wd_nccl_unique_id(char id[128]) {
+    Nccl& N = nccl();
+    if (!N.ok) return fail(WD_E_NCCL, "libnccl.so.2 not available");
+    ncclUniqueId u;
+    NK(N.GetUniqueId(&u));
+    memcpy(id, u.internal, 128);
+    return WD_OK;
+}
+
+int wd_nccl_comm_init(const char id[128], int nranks, int rank, void** comm) {
+    Nccl& N = nccl();
+    if (!N.ok) return fail(WD_E_NCCL, "libnccl.so.2 not available");
+    ncclUniqueId u;
+    memcpy(u.internal, id, 128);
+    ncclComm_t c;
+    NK(N.CommInitRank(&c, nranks, u, rank));
+    *comm = c;
+    return WD_OK;
+}
+
+void wd_partition_rows(int n2, int nranks, int rank, int* j_begin, int* j_end) {
+    *j_begin = (int)((long long)n2 * rank / nranks);
+    *j_end = (int)((long long)n2 * (rank + 1) / nranks);
+}
+
 static int assemble_impl(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
-                         double a1, double a2, double a3, const wd_options* opt,
-                         cudaStream_t st, wd_ctx* ctx) {
-    int rc;
+                         double a1, double a2, double a3, const wd_options* opt, cudaStream_t st,
+                         wd_ctx* ctx) {
     ctx->n1 = n1;
     ctx->n2 = n2;
     ctx->n3 = n3;
@@ -517,142 +841,338 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
     for (int d = 0; d < 3; d++) ctx->c[d] = 1.0 / (ctx->a[d] * ctx->a[d]);
     if (opt) ctx->opt = *opt;
     else wd_default_options(&ctx->opt);
-    const size_t N = (size_t)n1 * n2 * n3;
-    // internal copies of the coordinates (natural layout)
-    Stage sx, sy, sz;
-    if ((rc = stage_in(nullptr, sx, X, N, st)) || (rc = stage_in(nullptr, sy, Y, N, st)) ||
-        (rc = stage_in(nullptr, sz, Z, N, st)))
-        return rc;
-    if ((rc = dalloc(ctx, (void**)&ctx->X, sizeof(double) * N))) return rc;
-    if ((rc = dalloc(ctx, (void**)&ctx->Y, sizeof(double) * N))) return rc;
-    if ((rc = dalloc(ctx, (void**)&ctx->Z, sizeof(double) * N))) return rc;
-    CK(cudaMemcpyAsync(ctx->X, sx.d, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(ctx->Y, sy.d, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(ctx->Z, sz.d, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
-    if ((rc = stage_finish(st, {&sx, &sy, &sz}))) return rc;
+    const wd_options& o = ctx->opt;
+    // ---- decomposition
+    ctx->nranks = o.nranks > 1 ? o.nranks : 1;
+    if (ctx->nranks == 1) ctx->mode = MODE_SINGLE;
+    else if (o.rank < 0) ctx->mode = MODE_VIRTUAL;
+    else ctx->mode = MODE_NCCL;
+    if (ctx->nranks > 64) return fail(WD_E_INVAL, "nranks %d > 64", ctx->nranks);
+    ctx->own0g.resize(ctx->nranks);
+    ctx->own1g.resize(ctx->nranks);
+    if (ctx->mode == MODE_NCCL) {
+        if (!o.nccl_comm) return fail(WD_E_INVAL, "NCCL mode needs opt.nccl_comm (wd_nccl_comm_init)");
+        if (!nccl().ok) return fail(WD_E_NCCL, "libnccl.so.2 not available");
+        ctx->comm = (ncclComm_t)o.nccl_comm;
+        ctx->rank = o.rank;
+    }
+    for (int r = 0; r < ctx->nranks; r++) wd_partition_rows(n2, ctx->nranks, r, &ctx->own0g[r], &ctx->own1g[r]);
+    if (ctx->mode == MODE_NCCL && (o.j_begin != ctx->own0g[o.rank] || o.j_end != ctx->own1g[o.rank]))
+        return fail(WD_E_INVAL, "rank %d: rows [%d,%d) differ from wd_partition_rows [%d,%d)", o.rank,
+                    o.j_begin, o.j_end, ctx->own0g[o.rank], ctx->own1g[o.rank]);
+    for (int r = 0; r < ctx->nranks; r++)
+        if (ctx->own1g[r] - ctx->own0g[r] < MIN_OWNED)
+            return fail(WD_E_INVAL, "rank %d owns %d rows (< %d)", r, ctx->own1g[r] - ctx->own0g[r], MIN_OWNED);
+    const int nparts = ctx->mode == MODE_VIRTUAL ? ctx->nranks : 1;
+    ctx->parts.resize(nparts);
+    for (int p = 0; p < nparts; p++) {
+        Part& P = ctx->parts[p];
+        P.rank = ctx->mode == MODE_NCCL ? ctx->rank : p;
+        P.own0g = ctx->own0g[P.rank];
+        P.own1g = ctx->own1g[P.rank];
+        P.jlo = ctx->nranks > 1 ? std::max(P.own0g - HALO, 0) : 0;
+        P.jhi = ctx->nranks > 1 ? std::min(P.own1g + HALO, n2) : n2;
+    }
 
-    if ((rc = dalloc(ctx, (void**)&ctx->dscal, sizeof(double) * 4096))) return rc;
+    // ---- coordinates: internal copies of the part's rows (natural layout)
+    {
+        const size_t N = abi_nodes(ctx);
+        Stage sx, sy, sz;
+        RC(stage_in(nullptr, sx, X, N, st));
+        RC(stage_in(nullptr, sy, Y, N, st));
+        RC(stage_in(nullptr, sz, Z, N, st));
+        const int rows_in = ctx->mode == MODE_NCCL ? ctx->parts[0].jhi - ctx->parts[0].jlo : n2;
+        for (Part& P : ctx->parts) {
+            const int rows = P.jhi - P.jlo;
+            const size_t n = (size_t)n1 * rows * n3;
+            const int jofs = ctx->mode == MODE_NCCL ? 0 : P.jlo;
+            double** dst[3] = {&P.X, &P.Y, &P.Z};
+            const double* src[3] = {sx.d, sy.d, sz.d};
+            for (int d = 0; d < 3; d++) {
+                RC(dalloc(ctx, (void**)dst[d], sizeof(double) * n));
+                CK(cudaMemcpy2DAsync(*dst[d], sizeof(double) * n1 * rows,
+                                     src[d] + (size_t)jofs * n1, sizeof(double) * n1 * rows_in,
+                                     sizeof(double) * n1 * rows, n3, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        RC(stage_finish(st, {&sx, &sy, &sz}));
+    }
+    RC(dalloc(ctx, (void**)&ctx->dscal, sizeof(double) * 4096));
     CK(cudaMallocHost((void**)&ctx->hscal, sizeof(double) * 64));
     CK(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
     apply_tma_prepare();
-    if (ctx->opt.profile) {
+    if (o.profile) {
         for (auto& e : ctx->ev_gs) CK(cudaEventCreate(&e));
         for (auto& e : ctx->ev_cyc) CK(cudaEventCreate(&e));
         for (auto& e : ctx->ev_res) CK(cudaEventCreate(&e));
     }
 
-    // level 0: assembly fused with validation
-    Level& L0 = ctx->lev[0];
-    if ((rc = alloc_level(ctx, L0, n1, n2, n3))) return rc;
+    // ---- level 0: assembly fused with validation
+    const bool multi = ctx->nranks > 1;
+    unsigned long long* dbad = (unsigned long long*)(ctx->dscal + 8);
+    unsigned long long worst = ~0ull;
+    int wei = 0, wej = 0, wek = 0;
+    for (Part& P : ctx->parts) {
+        Level& L0 = P.lev[0];
+        const int rows = P.jhi - P.jlo;
+        L0.L = make_level(n1, rows, n3, P.jlo, n2, P.own0g - P.jlo, P.own1g - P.jlo);
+        L0.dist = multi;
+        L0.cown0 = L0.L.own0;
+        L0.cown1 = L0.L.own1;
+        RC(alloc_level(ctx, L0));
+        CK(cudaMemsetAsync(dbad, 0xff, sizeof(unsigned long long), st));
+        launch_assemble(P.X, P.Y, P.Z, n1, rows, n3, ctx->c, L0.L, L0.coef, dbad, st);
+        CKL();
+        unsigned long long hb;
+        CK(cudaMemcpyAsync(&hb, dbad, sizeof hb, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (hb != ~0ull) {
+            const unsigned long long e = hb / 16;
+            const int nx = n1 - 1, nyl = rows - 1;
+            const int ei = (int)(e % nx), ej = (int)((e / nx) % nyl) + P.jlo,
+                      ek = (int)(e / ((unsigned long long)nx * nyl));
+            const unsigned long long g = (((unsigned long long)ek * (n2 - 1) + ej) * nx + ei) * 16 + hb % 16;
+            if (g < worst) { worst = g; wei = ei; wej = ej; wek = ek; }
+        }
+        int cnt = (((n1 + 1) / 2 + 31) / 32) * ((rows + 3) / 4) + 4096;
+        P.npartial = cnt;
+        RC(dalloc(ctx, (void**)&P.partial, sizeof(double) * cnt));
+    }
     ctx->nlev = 1;
-    unsigned long long* dbad = (unsigned long long*)ctx->dscal;
-    CK(cudaMemsetAsync(dbad, 0xff, sizeof(unsigned long long), st));
-    launch_assemble(ctx->X, ctx->Y, ctx->Z, n1, n2, n3, ctx->c, L0.L, L0.coef, dbad, st);
-    CKL();
-    unsigned long long hbad;
-    CK(cudaMemcpyAsync(&hbad, dbad, sizeof hbad, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (hbad != ~0ull) {
-        const unsigned long long e = hbad / 16, what = hbad % 16;
-        const int nx = n1 - 1, ny = n2 - 1;
-        const int ei = (int)(e % nx), ej = (int)((e / nx) % ny), ek = (int)(e / ((unsigned long long)nx * ny));
-        if (what == 0)
-            return fail(WD_E_MESH, "element (%d,%d,%d): Z not increasing in k", ei, ej, ek);
-        return fail(WD_E_MESH, "element (%d,%d,%d): detJ <= 0 at Gauss point %d", ei, ej, ek,
+    ctx->levdims[0][0] = n1;
+    ctx->levdims[0][1] = n2;
+    ctx->levdims[0][2] = n3;
+    ctx->rrows.assign(1, std::vector<std::pair<int, int>>(ctx->nranks));
+    for (int r = 0; r < ctx->nranks; r++) ctx->rrows[0][r] = {ctx->own0g[r], ctx->own1g[r]};
+    if (ctx->mode == MODE_NCCL) {   // agree on the lowest failing element
+        unsigned long long* d = (unsigned long long*)(ctx->dscal + 16);
+        CK(cudaMemcpyAsync(d, &worst, sizeof worst, cudaMemcpyHostToDevice, st));
+        NK(nccl().AllReduce(d, d, 1, ncclUint64, ncclMin, ctx->comm, st));
+        unsigned long long g;
+        CK(cudaMemcpyAsync(&g, d, sizeof g, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (g != worst) {
+            worst = g;
+            const unsigned long long e = g / 16;
+            wei = (int)(e % (n1 - 1));
+            wej = (int)((e / (n1 - 1)) % (n2 - 1));
+            wek = (int)(e / ((unsigned long long)(n1 - 1) * (n2 - 1)));
+        }
+    }
+    if (worst != ~0ull) {
+        const unsigned long long what = worst % 16;
+        if (what == 0) return fail(WD_E_MESH, "element (%d,%d,%d): Z not increasing in k", wei, wej, wek);
+        return fail(WD_E_MESH, "element (%d,%d,%d): detJ <= 0 at Gauss point %d", wei, wej, wek,
                     (int)what - 1);
     }
+    RC(exchange(ctx, 0, ARR_COEF, HALO, st));   // rows at the slab edges come from the neighbours
 
-    // planner inputs (reading C2): h1 = sqrt(dx dy); h3 at the column of minimum Z(i,j,0)
-    double h[2], org[2];
-    CK(cudaMemcpy(&org[0], ctx->X, sizeof(double), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&h[0], ctx->X + 1, sizeof(double), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&org[1], ctx->Y, sizeof(double), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&h[1], ctx->Y + n1, sizeof(double), cudaMemcpyDeviceToHost));
-    double h1 = std::sqrt((h[0] - org[0]) * (h[1] - org[1]));
+    // ---- planner inputs (reading C2): h1 = sqrt(dx dy); h3 at the column of minimum Z(i,j,0)
+    double h1;
+    double h3[MAXNZ], h3n[MAXNZ], h1n;
     {
+        Part& P0 = ctx->parts[0];
+        double v[4];
+        CK(cudaMemcpy(&v[0], P0.X, sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&v[1], P0.X + 1, sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&v[2], P0.Y, sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&v[3], P0.Y + n1, sizeof(double), cudaMemcpyDeviceToHost));
+        h1 = std::sqrt((v[1] - v[0]) * (v[3] - v[2]));
+        if (ctx->mode == MODE_NCCL) {   // every rank plans with rank 0's (global origin) h1
+            double* dh = ctx->dscal + 2040;
+            CK(cudaMemcpyAsync(dh, &h1, sizeof h1, cudaMemcpyHostToDevice, st));
+            NK(nccl().Bcast(dh, dh, 1, ncclDouble, 0, ctx->comm, st));
+            CK(cudaMemcpyAsync(&h1, dh, sizeof h1, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+        // every part: argmin over its owned bottom rows -> (value, global index)
         const int nblk = 256;
-        double* pval = ctx->dscal + 16;
-        long long* pidx = (long long*)(ctx->dscal + 16 + 2 * (nblk + 1));
-        launch_argmin_bottom(ctx->Z, n1 * n2, pval, pidx, nblk, st);
-        CKL();
-        long long best;
-        CK(cudaMemcpyAsync(&best, pidx + nblk, sizeof best, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        double* pval = ctx->dscal + 1024;
+        long long* pidx = (long long*)(ctx->dscal + 1024 + 2 * (nblk + 1));
+        double best = 0.0;
+        long long bidx = -1;
+        int bpart = 0;
+        std::vector<double> cand_v;
+        std::vector<long long> cand_i;
+        for (size_t p = 0; p < ctx->parts.size(); p++) {
+            Part& P = ctx->parts[p];
+            const int o0 = P.lev[0].L.own0, o1 = P.lev[0].L.own1;
+            launch_argmin_bottom(P.Z + (size_t)o0 * n1, (o1 - o0) * n1, pval, pidx, nblk, st);
+            CKL();
+            double hv;
+            long long hi;
+            CK(cudaMemcpyAsync(&hv, pval + nblk, sizeof hv, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(&hi, pidx + nblk, sizeof hi, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            const long long gi = hi + (long long)P.own0g * n1;   // global bottom index
+            if (bidx < 0 || hv < best || (hv == best && gi < bidx)) { best = hv; bidx = gi; bpart = (int)p; }
+        }
         std::vector<double> zc(n3);
-        for (int k = 0; k < n3; k++)
-            CK(cudaMemcpy(&zc[k], ctx->Z + (size_t)k * n1 * n2 + best, sizeof(double),
-                          cudaMemcpyDeviceToHost));
-        double h3[MAXNZ], h3n[MAXNZ], h1n;
+        if (ctx->mode == MODE_NCCL) {
+            // agree on (value, index): all-gather both, pick the minimum
+            double* dv = ctx->dscal + 2048;
+            double mine[2] = {best, (double)bidx};
+            CK(cudaMemcpyAsync(dv, mine, sizeof mine, cudaMemcpyHostToDevice, st));
+            NK(nccl().AllGather(dv, dv + 2, 2, ncclDouble, ctx->comm, st));
+            std::vector<double> all(2 * ctx->nranks);
+            CK(cudaMemcpyAsync(all.data(), dv + 2, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            int win = 0;
+            for (int r = 1; r < ctx->nranks; r++)
+                if (all[2 * r] < all[2 * win] || (all[2 * r] == all[2 * win] && all[2 * r + 1] < all[2 * win + 1]))
+                    win = r;
+            bidx = (long long)all[2 * win + 1];
+            // the winner broadcasts its column
+            double* col = ctx->dscal + 2560;
+            if (win == ctx->rank) {
+                Part& P = ctx->parts[0];
+                const long long li = bidx - (long long)P.jlo * n1;
+                for (int k = 0; k < n3; k++)
+                    CK(cudaMemcpyAsync(col + k, P.Z + (size_t)k * n1 * (P.jhi - P.jlo) + li, sizeof(double),
+                                       cudaMemcpyDeviceToDevice, st));
+            }
+            NK(nccl().Bcast(col, col, n3, ncclDouble, win, ctx->comm, st));
+            CK(cudaMemcpyAsync(zc.data(), col, sizeof(double) * n3, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        } else {
+            Part& P = ctx->parts[bpart];
+            const long long li = bidx - (long long)P.jlo * n1;
+            for (int k = 0; k < n3; k++)
+                CK(cudaMemcpy(&zc[k], P.Z + (size_t)k * n1 * (P.jhi - P.jlo) + li, sizeof(double),
+                              cudaMemcpyDeviceToHost));
+        }
         for (int k = 0; k + 1 < n3; k++) h3[k] = zc[k + 1] - zc[k];
-        // hierarchy
-        while (ctx->nlev < MAXLEV) {
-            Level& F = ctx->lev[ctx->nlev - 1];
-            if (level_free(F.L) <= ctx->opt.coarsest_max_free) break;
-            int hflag;
-            if (!plan_level(h1, h3, F.L.n3 - 1, ctx->a, ctx->opt.coarsen_rule, F.L.n1, F.L.n2,
-                            &hflag, F.kept, &F.nkept, &h1n, h3n))
-                break;
+    }
+
+    // ---- hierarchy
+    while (ctx->nlev < MAXLEV) {
+        const int l = ctx->nlev - 1;
+        const int fn1 = ctx->levdims[l][0], fn2 = ctx->levdims[l][1], fn3 = ctx->levdims[l][2];
+        if (free_count(fn1, fn2, fn3) <= o.coarsest_max_free) break;
+        int hflag, kept[MAXNZ], nk;
+        if (!plan_level(h1, h3, fn3 - 1, ctx->a, o.coarsen_rule, fn1, fn2, &hflag, kept, &nk, &h1n, h3n))
+            break;
+        std::vector<int> px(fn1), py(fn2);
+        int m1, m2;
+        if (hflag) {
+            m1 = horiz_kept(fn1, px.data());
+            m2 = horiz_kept(fn2, py.data());
+        } else {
+            m1 = fn1;
+            m2 = fn2;
+            for (int t = 0; t < m1; t++) px[t] = t;
+            for (int t = 0; t < m2; t++) py[t] = t;
+        }
+        px.resize(m1);
+        py.resize(m2);
+        const int cl = l + 1;
+        ctx->levdims[cl][0] = m1;
+        ctx->levdims[cl][1] = m2;
+        ctx->levdims[cl][2] = nk;
+        // gather decision (multi-rank): replicate the coarse level when it is
+        // small or when a rank would own fewer than MIN_OWNED rows of it
+        bool coarse_dist = false;
+        ctx->rrows.resize(cl + 1);
+        ctx->rrows[cl].resize(ctx->nranks);
+        for (int r = 0; r < ctx->nranks; r++) {
+            int a = 0, b = m2;
+            if (l < ctx->gather) coarse_range(py, ctx->rrows[l][r].first, ctx->rrows[l][r].second, a, b);
+            ctx->rrows[cl][r] = {a, b};
+        }
+        if (multi && ctx->gather == MAXLEV) {
+            coarse_dist = (long long)m1 * m2 * nk >= o.gather_below_nodes;
+            for (int r = 0; r < ctx->nranks; r++)
+                if (ctx->rrows[cl][r].second - ctx->rrows[cl][r].first < MIN_OWNED) coarse_dist = false;
+            if (!coarse_dist) ctx->gather = cl;
+        }
+        for (Part& P : ctx->parts) {
+            Level& F = P.lev[l];
             F.hflag = hflag;
-            std::vector<int> px(F.L.n1), py(F.L.n2);
-            int m1, m2;
-            if (hflag) {
-                m1 = horiz_kept(F.L.n1, px.data());
-                m2 = horiz_kept(F.L.n2, py.data());
+            F.nkept = nk;
+            for (int t = 0; t < nk; t++) F.kept[t] = kept[t];
+            Level& C = P.lev[cl];
+            // coarse rows this part owns / computes
+            int c0, c1;
+            coarse_range(py, F.L.jg0 + F.L.own0, F.L.jg0 + F.L.own1, c0, c1);
+            if (!F.dist) { c0 = 0; c1 = m2; }   // replicated fine level: everything
+            int jlo_c, jhi_c;
+            if (coarse_dist) {
+                jlo_c = std::max(c0 - HALO, 0);
+                jhi_c = std::min(c1 + HALO, m2);
+                C.L = make_level(m1, jhi_c - jlo_c, nk, jlo_c, m2, c0 - jlo_c, c1 - jlo_c);
+                C.dist = true;
+                C.cown0 = C.L.own0;
+                C.cown1 = C.L.own1;
             } else {
-                m1 = F.L.n1;
-                m2 = F.L.n2;
-                for (int t = 0; t < m1; t++) px[t] = t;
-                for (int t = 0; t < m2; t++) py[t] = t;
+                jlo_c = 0;
+                jhi_c = m2;
+                C.L = make_level(m1, m2, nk, 0, m2, 0, m2);
+                C.dist = false;
+                C.cown0 = c0;   // slice this part computes before the gather
+                C.cown1 = c1;
             }
-            const int nd[3] = {F.L.n1, F.L.n2, F.L.n3};
-            const int md[3] = {m1, m2, F.nkept};
-            const int* pos[3] = {px.data(), py.data(), F.kept};
-            size_t tot = 0;
-            for (int d = 0; d < 3; d++) tot += 2 * nd[d] + md[d];
-            std::vector<int> hmap(tot);
-            size_t offs[3][3], o = 0;
-            for (int d = 0; d < 3; d++) {
-                offs[d][0] = o;
-                offs[d][1] = o + nd[d];
-                offs[d][2] = o + 2 * nd[d];
-                map1d(nd[d], pos[d], md[d], &hmap[o], &hmap[o + nd[d]]);
-                for (int c = 0; c < md[d]; c++) hmap[o + 2 * nd[d] + c] = pos[d][c];
-                o += 2 * nd[d] + md[d];
+            RC(alloc_level(ctx, C));
+            // maps: x and z global; y local to the part (fine rows F.jg0.., coarse rows jlo_c..)
+            const int fr = F.L.n2, cr = C.L.n2;
+            std::vector<int> glo(fn2), gco(fn2), xlo(fn1), xco(fn1), zlo(fn3), zco(fn3);
+            map1d(fn1, px.data(), m1, xlo.data(), xco.data());
+            map1d(fn2, py.data(), m2, glo.data(), gco.data());
+            map1d(fn3, kept, nk, zlo.data(), zco.data());
+            std::vector<int> hmap;
+            size_t offs[3][3];
+            auto put = [&](int d, const int* lo, const int* co, int n, const int* pos, int m) {
+                offs[d][0] = hmap.size();
+                hmap.insert(hmap.end(), lo, lo + n);
+                offs[d][1] = hmap.size();
+                hmap.insert(hmap.end(), co, co + n);
+                offs[d][2] = hmap.size();
+                hmap.insert(hmap.end(), pos, pos + m);
+            };
+            std::vector<int> ylo(fr), yco(fr), ypos(cr);
+            for (int t = 0; t < fr; t++) {
+                const int g = t + F.L.jg0;
+                ylo[t] = glo[g] - jlo_c;
+                yco[t] = gco[g];
             }
-            if ((rc = dalloc(ctx, (void**)&F.dmap, sizeof(int) * tot))) return rc;
-            CK(cudaMemcpy(F.dmap, hmap.data(), sizeof(int) * tot, cudaMemcpyHostToDevice));
+            for (int cc = 0; cc < cr; cc++) ypos[cc] = py[cc + jlo_c] - F.L.jg0;
+            put(0, xlo.data(), xco.data(), fn1, px.data(), m1);
+            put(1, ylo.data(), yco.data(), fr, ypos.data(), cr);
+            put(2, zlo.data(), zco.data(), fn3, kept, nk);
+            RC(dalloc(ctx, (void**)&F.dmap, sizeof(int) * hmap.size()));
+            CK(cudaMemcpy(F.dmap, hmap.data(), sizeof(int) * hmap.size(), cudaMemcpyHostToDevice));
             for (int d = 0; d < 3; d++) {
                 F.M.lo[d] = F.dmap + offs[d][0];
                 F.M.co[d] = F.dmap + offs[d][1];
                 F.M.pos[d] = F.dmap + offs[d][2];
             }
-            Level& C = ctx->lev[ctx->nlev];
-            if ((rc = alloc_level(ctx, C, m1, m2, F.nkept))) return rc;
-            ctx->nlev++;
-            launch_galerkin(F.L, C.L, F.M, F.coef, C.coef, nullptr, st);
+            launch_galerkin(F.L, target(C), F.M, F.coef, C.coef, nullptr, st);
             CKL();
-            h1 = h1n;
-            for (int t = 0; t + 1 < F.nkept; t++) h3[t] = h3n[t];
         }
+        ctx->nlev++;
+        if (coarse_dist) RC(exchange(ctx, cl, ARR_COEF, HALO, st));
+        else if (cl == ctx->gather) RC(gather_rows(ctx, cl, ARR_COEF, st));
+        h1 = h1n;
+        for (int t = 0; t + 1 < nk; t++) h3[t] = h3n[t];
     }
-    // coarsest level (reading C8)
-    Level& Lc = ctx->lev[ctx->nlev - 1];
-    const i64 nf = level_free(Lc.L);
-    ctx->nf = (int)nf;
-    ctx->coarse_direct = nf <= ctx->opt.coarsest_max_free;
-    if (ctx->coarse_direct && nf > 0) {
-        if ((rc = dalloc(ctx, (void**)&ctx->Ainv, sizeof(double) * (size_t)nf * nf))) return rc;
-        if ((rc = dalloc(ctx, (void**)&ctx->Dinv, sizeof(double) * 32 * 32))) return rc;
-        coarse_prepare((int)nf);
-        launch_dense_build(Lc.L, Lc.coef, ctx->Ainv, (int)nf, st);
-        gj_invert(ctx->Ainv, (int)nf, ctx->Dinv, st);
-        CKL();
-    }
-    // partial-sum scratch: enough for the apply grid of level 0 and the norm kernel
+    // ---- coarsest level (reading C8): replicated or single
     {
-        const LevDev& L = L0.L;
-        ctx->npartial = ((L.n1 + 1) / 2 + 127) / 128 * L.n2 * 2 + 2048;
-        if ((rc = dalloc(ctx, (void**)&ctx->partial, sizeof(double) * ctx->npartial))) return rc;
+        const int l = ctx->nlev - 1;
+        const int* d = ctx->levdims[l];
+        const i64 nf = free_count(d[0], d[1], d[2]);
+        ctx->nf = (int)nf;
+        ctx->coarse_direct = nf <= o.coarsest_max_free;
+        if (ctx->parts[0].lev[l].dist && ctx->coarse_direct)
+            return fail(WD_E_INTERNAL, "coarsest level is distributed (raise gather_below_nodes)");
+        if (ctx->coarse_direct && nf > 0) {
+            coarse_prepare((int)nf);
+            for (Part& P : ctx->parts) {
+                RC(dalloc(ctx, (void**)&P.Ainv, sizeof(double) * (size_t)nf * nf));
+                RC(dalloc(ctx, (void**)&P.Dinv, sizeof(double) * 32 * 32));
+                launch_dense_build(P.lev[l].L, P.lev[l].coef, P.Ainv, (int)nf, st);
+                gj_invert(P.Ainv, (int)nf, P.Dinv, st);
+                CKL();
+            }
+        }
     }
     CK(cudaStreamSynchronize(st));
     CKL();
@@ -683,10 +1203,12 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
         memcpy(keep, g_err, sizeof keep);
         cudaStreamSynchronize((cudaStream_t)stream);
         cudaGetLastError();
+        ctx->comm = nullptr;   // owned by the caller
         wd_destroy(ctx);
         memcpy(g_err, keep, sizeof keep);
         return rc;
     }
+    if (ctx->mode == MODE_NCCL) ctx->comm = (ncclComm_t)ctx->opt.nccl_comm;
     *out = ctx;
     return WD_OK;
 }
@@ -694,12 +1216,11 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
 int wd_rhs(wd_ctx* ctx, const double* u0, double* f, void* stream) {
     if (!ctx || !u0 || !f) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t E = (size_t)(ctx->n1 - 1) * (ctx->n2 - 1) * (ctx->n3 - 1);
-    const size_t N = (size_t)ctx->n1 * ctx->n2 * ctx->n3;
     Stage su, sf;
-    int rc;
-    if ((rc = stage_in(ctx, su, u0, 3 * E, st)) || (rc = stage_out(ctx, sf, f, N))) return rc;
-    launch_rhs(ctx->X, ctx->Y, ctx->Z, ctx->n1, ctx->n2, ctx->n3, su.d, sf.d, st);
+    RC(stage_in(ctx, su, u0, abi_elems(ctx), st));
+    RC(stage_out(ctx, sf, f, abi_nodes(ctx)));
+    for (Part& P : ctx->parts)
+        launch_rhs(P.X, P.Y, P.Z, P.lev[0].L, nat_elems(ctx, P, su.d), nat_nodes(ctx, P, sf.d), st);
     CKL();
     return stage_finish(st, {&su, &sf});
 }
@@ -707,14 +1228,13 @@ int wd_rhs(wd_ctx* ctx, const double* u0, double* f, void* stream) {
 int wd_recover_wind(wd_ctx* ctx, const double* lambda, const double* u0, double* u, void* stream) {
     if (!ctx || !lambda || !u0 || !u) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t E = (size_t)(ctx->n1 - 1) * (ctx->n2 - 1) * (ctx->n3 - 1);
-    const size_t N = (size_t)ctx->n1 * ctx->n2 * ctx->n3;
     Stage sl, su0, su;
-    int rc;
-    if ((rc = stage_in(ctx, sl, lambda, N, st)) || (rc = stage_in(ctx, su0, u0, 3 * E, st)) ||
-        (rc = stage_out(ctx, su, u, 3 * E)))
-        return rc;
-    launch_recover(ctx->X, ctx->Y, ctx->Z, ctx->n1, ctx->n2, ctx->n3, ctx->c, sl.d, su0.d, su.d, st);
+    RC(stage_in(ctx, sl, lambda, abi_nodes(ctx), st));
+    RC(stage_in(ctx, su0, u0, abi_elems(ctx), st));
+    RC(stage_out(ctx, su, u, abi_elems(ctx)));
+    for (Part& P : ctx->parts)
+        launch_recover(P.X, P.Y, P.Z, P.lev[0].L, ctx->c, nat_nodes(ctx, P, sl.d),
+                       nat_elems(ctx, P, su0.d), nat_elems(ctx, P, su.d), st);
     CKL();
     return stage_finish(st, {&sl, &su0, &su});
 }
@@ -722,31 +1242,29 @@ int wd_recover_wind(wd_ctx* ctx, const double* lambda, const double* u0, double*
 int wd_vcycle(wd_ctx* ctx, double* lambda, const double* f, double* rel_res_out, void* stream) {
     if (!ctx || !lambda || !f) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
-    Level& F = ctx->lev[0];
-    const size_t N = nodes_of(F.L);
-    Stage sl, sf, so;
-    int rc;
-    if ((rc = stage_in(ctx, sl, lambda, N, st)) || (rc = stage_in(ctx, sf, f, N, st))) return rc;
-    launch_nat2int(F.L, sf.d, F.f, true, st);
-    launch_nat2int(F.L, sl.d, F.lam, true, st);
+    Stage sl, sf;
+    RC(stage_in(ctx, sl, lambda, abi_nodes(ctx), st));
+    RC(stage_in(ctx, sf, f, abi_nodes(ctx), st));
+    for (Part& P : ctx->parts) {
+        launch_nat2int(P.lev[0].L, nat_nodes(ctx, P, sf.d), P.lev[0].f, true, st);
+        launch_nat2int(P.lev[0].L, nat_nodes(ctx, P, sl.d), P.lev[0].lam, true, st);
+    }
     CKL();
-    if ((rc = run_vcycle(ctx, st))) return rc;
+    RC(run_vcycle(ctx, st));
     if (rel_res_out) {
-        if ((rc = residual_sq(ctx, 0, st)) || (rc = norm_sq(ctx, F.L, F.f, 1, st)) ||
-            (rc = fetch_scalars(ctx, 2, st)))
-            return rc;
+        RC(residual_sq(ctx, 0, st));
+        RC(norm_sq(ctx, ARR_F, 1, st));
+        RC(fetch_scalars(ctx, 2, st));
         const double a = std::sqrt(ctx->hscal[0]), fn = std::sqrt(ctx->hscal[1]);
         *rel_res_out = fn > 0 ? a / fn : a;
         profile_accumulate(ctx, true, true);
     }
-    // write back (lambda may be host or device)
-    so = sl;
+    Stage so = sl;
     so.out = true;
     so.host = lambda;
-    launch_int2nat(F.L, F.lam, so.d, st);
+    out_nodes(ctx, so.d, st);
     CKL();
-    rc = stage_finish(st, {&so, &sf});
-    return rc;
+    return stage_finish(st, {&so, &sf});
 }
 
 int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol, double* lambda,
@@ -754,36 +1272,33 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
     if (!ctx || !f || !lambda) return fail(WD_E_INVAL, "NULL argument");
     if (!(rel_tol > 0.0 && rel_tol < 1.0)) return fail(WD_E_INVAL, "rel_tol must be in (0,1)");
     cudaStream_t st = (cudaStream_t)stream;
-    Level& F = ctx->lev[0];
-    const size_t N = nodes_of(F.L);
     Stage sf, s0, sl;
-    int rc;
-    if ((rc = stage_in(ctx, sf, f, N, st))) return rc;
-    if (lambda0 && (rc = stage_in(ctx, s0, lambda0, N, st))) return rc;
-    if ((rc = stage_out(ctx, sl, lambda, N))) return rc;
-    launch_nat2int(F.L, sf.d, F.f, true, st);
-    if (lambda0) launch_nat2int(F.L, s0.d, F.lam, true, st);
-    else CK(cudaMemsetAsync(F.lam, 0, sizeof(double) * F.L.NT, st));
+    RC(stage_in(ctx, sf, f, abi_nodes(ctx), st));
+    if (lambda0) RC(stage_in(ctx, s0, lambda0, abi_nodes(ctx), st));
+    RC(stage_out(ctx, sl, lambda, abi_nodes(ctx)));
+    for (Part& P : ctx->parts) {
+        Level& F = P.lev[0];
+        launch_nat2int(F.L, nat_nodes(ctx, P, sf.d), F.f, true, st);
+        if (lambda0) launch_nat2int(F.L, nat_nodes(ctx, P, s0.d), F.lam, true, st);
+        else CK(cudaMemsetAsync(F.lam, 0, sizeof(double) * F.L.NT, st));
+    }
     CKL();
     wd_report R;
     memset(&R, 0, sizeof R);
     R.nlevels = ctx->nlev;
-    for (int l = 0; l < ctx->nlev && l < 32; l++) {
-        R.dims[l][0] = ctx->lev[l].L.n1;
-        R.dims[l][1] = ctx->lev[l].L.n2;
-        R.dims[l][2] = ctx->lev[l].L.n3;
-    }
+    for (int l = 0; l < ctx->nlev && l < 32; l++)
+        for (int d = 0; d < 3; d++) R.dims[l][d] = ctx->levdims[l][d];
     R.coarse_direct = ctx->coarse_direct;
     R.coarse_free = ctx->nf;
-    if ((rc = norm_sq(ctx, F.L, F.f, 1, st)) || (rc = residual_sq(ctx, 0, st)) ||
-        (rc = fetch_scalars(ctx, 2, st)))
-        return rc;
+    RC(norm_sq(ctx, ARR_F, 1, st));
+    RC(residual_sq(ctx, 0, st));
+    RC(fetch_scalars(ctx, 2, st));
     profile_accumulate(ctx, false, true);
     const double fn = std::sqrt(ctx->hscal[1]);
     int status = WD_E_NOCONV;
     int c = 0;
     if (fn == 0.0) {
-        CK(cudaMemsetAsync(F.lam, 0, sizeof(double) * F.L.NT, st));
+        for (Part& P : ctx->parts) CK(cudaMemsetAsync(P.lev[0].lam, 0, sizeof(double) * P.lev[0].L.NT, st));
         R.rel_res_hist[0] = 0.0;
         status = WD_OK;
     } else {
@@ -793,9 +1308,9 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
         if (!std::isfinite(rel)) status = WD_E_NONFINITE;
         else if (rel <= rel_tol) status = WD_OK;
         while (status == WD_E_NOCONV && c < ctx->opt.max_cycles) {
-            if ((rc = run_vcycle(ctx, st)) || (rc = residual_sq(ctx, 0, st)) ||
-                (rc = fetch_scalars(ctx, 1, st)))
-                return rc;
+            RC(run_vcycle(ctx, st));
+            RC(residual_sq(ctx, 0, st));
+            RC(fetch_scalars(ctx, 1, st));
             c++;
             profile_accumulate(ctx, true, true);
             rel = std::sqrt(ctx->hscal[0]) / fn;
@@ -812,9 +1327,9 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
     R.rel_res_final = R.rel_res_hist[ch];
     if (c >= 2) R.rate = std::pow(R.rel_res_hist[ch] / R.rel_res_hist[1], 1.0 / (ch - 1));
     else if (c == 1) R.rate = R.rel_res_hist[1] / R.rel_res_hist[0];
-    launch_int2nat(F.L, F.lam, sl.d, st);
+    out_nodes(ctx, sl.d, st);
     CKL();
-    if ((rc = stage_finish(st, {&sf, &s0, &sl}))) return rc;
+    RC(stage_finish(st, {&sf, &s0, &sl}));
     if (rep) *rep = R;
     if (status == WD_E_NOCONV) return fail(WD_E_NOCONV, "not converged after %d cycles (rel %.3e)", c, R.rel_res_final);
     if (status == WD_E_DIVERGED) return fail(WD_E_DIVERGED, "diverged at cycle %d", c);
@@ -838,13 +1353,14 @@ void wd_profile_reset(wd_ctx* ctx) {
 long long wd_launch_count(void) { return g_launches.load(); }
 
 int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out) {
-    int rc = check_level(ctx, level);
-    if (rc) return rc;
+    RC(check_level(ctx, level));
+    RC(check_single(ctx));
     if (reps < 1 || !ms_out) return fail(WD_E_INVAL, "reps < 1 or NULL output");
     if ((which == 2 || which == 3 || which == 6) && level >= ctx->nlev - 1)
         return fail(WD_E_INVAL, "no coarser level");
     cudaStream_t st = ctx->cap;
-    Level& F = ctx->lev[level];
+    Part& P = ctx->parts[0];
+    Level& F = P.lev[level];
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -852,25 +1368,24 @@ int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out)
         switch (which) {
             case 0: launch_gs_sweep(F.L, F.coef, F.lam, F.f, st); break;
             case 1: apply_level(F, true, nullptr, st); break;
-            case 2: launch_restrict(F.L, ctx->lev[level + 1].L, F.M, F.r, ctx->lev[level + 1].f, st); break;
-            case 3: launch_prolong(F.L, ctx->lev[level + 1].L, F.M, ctx->lev[level + 1].lam, F.lam, st); break;
+            case 2: launch_restrict(F.L, target(P.lev[level + 1]), F.M, F.r, P.lev[level + 1].f, st); break;
+            case 3: launch_prolong(F.L, P.lev[level + 1].L, F.M, P.lev[level + 1].lam, F.lam, st); break;
             case 4: return run_vcycle(ctx, st);
             case 5: return residual_sq(ctx, 0, st);
-            case 6: launch_galerkin(F.L, ctx->lev[level + 1].L, F.M, F.coef, ctx->lev[level + 1].coef, nullptr, st); break;
+            case 6: launch_galerkin(F.L, target(P.lev[level + 1]), F.M, F.coef, P.lev[level + 1].coef, nullptr, st); break;
             case 7: {
                 unsigned long long* dbad = (unsigned long long*)(ctx->dscal + 8);
-                launch_assemble(ctx->X, ctx->Y, ctx->Z, ctx->n1, ctx->n2, ctx->n3, ctx->c,
-                                ctx->lev[0].L, ctx->lev[0].coef, dbad, st);
+                launch_assemble(P.X, P.Y, P.Z, ctx->n1, ctx->n2, ctx->n3, ctx->c, P.lev[0].L,
+                                P.lev[0].coef, dbad, st);
                 break;
             }
             default: return fail(WD_E_INVAL, "unknown kernel %d", which);
         }
         return WD_OK;
     };
-    if ((rc = body())) return rc;   // warm-up
+    RC(body());   // warm-up
     CK(cudaEventRecord(e0, st));
-    for (int r = 0; r < reps; r++)
-        if ((rc = body())) return rc;
+    for (int r = 0; r < reps; r++) RC(body());
     CK(cudaEventRecord(e1, st));
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -886,120 +1401,130 @@ int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out)
 int wd_num_levels(const wd_ctx* ctx) { return ctx ? ctx->nlev : 0; }
 
 int wd_level_dims(const wd_ctx* ctx, int level, int dims[3]) {
-    int rc = check_level(ctx, level);
-    if (rc) return rc;
-    dims[0] = ctx->lev[level].L.n1;
-    dims[1] = ctx->lev[level].L.n2;
-    dims[2] = ctx->lev[level].L.n3;
+    RC(check_level(ctx, level));
+    for (int d = 0; d < 3; d++) dims[d] = ctx->levdims[level][d];
     return WD_OK;
 }
 
 int wd_level_plan(const wd_ctx* ctx, int level, int* horizontal, int* kept, int* nkept) {
-    int rc = check_level(ctx, level);
-    if (rc) return rc;
+    RC(check_level(ctx, level));
     if (level >= ctx->nlev - 1) return fail(WD_E_INVAL, "level %d is the coarsest", level);
-    *horizontal = ctx->lev[level].hflag;
-    *nkept = ctx->lev[level].nkept;
-    for (int t = 0; t < ctx->lev[level].nkept; t++) kept[t] = ctx->lev[level].kept[t];
+    const Level& lv = ctx->parts[0].lev[level];
+    *horizontal = lv.hflag;
+    *nkept = lv.nkept;
+    for (int t = 0; t < lv.nkept; t++) kept[t] = lv.kept[t];
     return WD_OK;
 }
 
+int wd_gather_level(const wd_ctx* ctx) { return ctx ? (ctx->gather < MAXLEV ? ctx->gather : -1) : -1; }
+
 int wd_get_stencil(wd_ctx* ctx, int level, double* K27, void* stream) {
-    int rc = check_level(ctx, level);
-    if (rc) return rc;
+    RC(check_level(ctx, level));
+    RC(check_single(ctx));
     cudaStream_t st = (cudaStream_t)stream;
-    Level& lv = ctx->lev[level];
+    Level& lv = ctx->parts[0].lev[level];
     Stage so;
-    if ((rc = stage_out(ctx, so, K27, 27 * nodes_of(lv.L)))) return rc;
+    RC(stage_out(ctx, so, K27, 27 * nodes_of(lv.L)));
     launch_export27(lv.L, lv.coef, so.d, st);
     CKL();
     return stage_finish(st, {&so});
 }
 
+static Nat whole(const LevDev& L, const double* p) {
+    Nat a;
+    a.p = p;
+    a.n2a = L.n2;
+    a.jofs = 0;
+    return a;
+}
+
 int wd_apply(wd_ctx* ctx, int level, const double* x, double* y, void* stream) {
-    int rc = check_level(ctx, level);
-    if (rc) return rc;
+    RC(check_level(ctx, level));
+    RC(check_single(ctx));
     cudaStream_t st = (cudaStream_t)stream;
-    Level& lv = ctx->lev[level];
+    Level& lv = ctx->parts[0].lev[level];
     const size_t N = nodes_of(lv.L);
     Stage sx, sy;
-    if ((rc = stage_in(ctx, sx, x, N, st)) || (rc = stage_out(ctx, sy, y, N))) return rc;
-    launch_nat2int(lv.L, sx.d, lv.lam, true, st);
+    RC(stage_in(ctx, sx, x, N, st));
+    RC(stage_out(ctx, sy, y, N));
+    launch_nat2int(lv.L, whole(lv.L, sx.d), lv.lam, true, st);
     CK(cudaMemsetAsync(lv.r, 0, sizeof(double) * lv.L.NT, st));
     apply_level(lv, false, nullptr, st);
-    launch_int2nat(lv.L, lv.r, sy.d, st);
+    launch_int2nat(lv.L, lv.r, whole(lv.L, sy.d), st);
     CKL();
     return stage_finish(st, {&sx, &sy});
 }
 
 int wd_smooth(wd_ctx* ctx, int level, double* x, const double* f, int sweeps, void* stream) {
-    int rc = check_level(ctx, level);
-    if (rc) return rc;
+    RC(check_level(ctx, level));
+    RC(check_single(ctx));
     cudaStream_t st = (cudaStream_t)stream;
-    Level& lv = ctx->lev[level];
+    Level& lv = ctx->parts[0].lev[level];
     const size_t N = nodes_of(lv.L);
     Stage sx, sf;
-    if ((rc = stage_in(ctx, sx, x, N, st)) || (rc = stage_in(ctx, sf, f, N, st))) return rc;
-    launch_nat2int(lv.L, sx.d, lv.lam, true, st);
-    launch_nat2int(lv.L, sf.d, lv.f, true, st);
+    RC(stage_in(ctx, sx, x, N, st));
+    RC(stage_in(ctx, sf, f, N, st));
+    launch_nat2int(lv.L, whole(lv.L, sx.d), lv.lam, true, st);
+    launch_nat2int(lv.L, whole(lv.L, sf.d), lv.f, true, st);
     for (int s = 0; s < sweeps; s++) launch_gs_sweep(lv.L, lv.coef, lv.lam, lv.f, st);
     sx.out = true;
     sx.host = x;
-    launch_int2nat(lv.L, lv.lam, sx.d, st);
+    launch_int2nat(lv.L, lv.lam, whole(lv.L, sx.d), st);
     CKL();
     return stage_finish(st, {&sx, &sf});
 }
 
 int wd_restrict(wd_ctx* ctx, int level, const double* r, double* fc, void* stream) {
-    int rc = check_level(ctx, level);
-    if (rc) return rc;
+    RC(check_level(ctx, level));
+    RC(check_single(ctx));
     if (level >= ctx->nlev - 1) return fail(WD_E_INVAL, "no coarser level");
     cudaStream_t st = (cudaStream_t)stream;
-    Level& F = ctx->lev[level];
-    Level& C = ctx->lev[level + 1];
+    Level& F = ctx->parts[0].lev[level];
+    Level& C = ctx->parts[0].lev[level + 1];
     Stage sr, sc;
-    if ((rc = stage_in(ctx, sr, r, nodes_of(F.L), st)) || (rc = stage_out(ctx, sc, fc, nodes_of(C.L))))
-        return rc;
-    launch_nat2int(F.L, sr.d, F.r, true, st);
+    RC(stage_in(ctx, sr, r, nodes_of(F.L), st));
+    RC(stage_out(ctx, sc, fc, nodes_of(C.L)));
+    launch_nat2int(F.L, whole(F.L, sr.d), F.r, true, st);
     CK(cudaMemsetAsync(C.f, 0, sizeof(double) * C.L.NT, st));
-    launch_restrict(F.L, C.L, F.M, F.r, C.f, st);
-    launch_int2nat(C.L, C.f, sc.d, st);
+    launch_restrict(F.L, target(C), F.M, F.r, C.f, st);
+    launch_int2nat(C.L, C.f, whole(C.L, sc.d), st);
     CKL();
     return stage_finish(st, {&sr, &sc});
 }
 
 int wd_prolong(wd_ctx* ctx, int level, const double* xc, double* x, void* stream) {
-    int rc = check_level(ctx, level);
-    if (rc) return rc;
+    RC(check_level(ctx, level));
+    RC(check_single(ctx));
     if (level >= ctx->nlev - 1) return fail(WD_E_INVAL, "no coarser level");
     cudaStream_t st = (cudaStream_t)stream;
-    Level& F = ctx->lev[level];
-    Level& C = ctx->lev[level + 1];
+    Level& F = ctx->parts[0].lev[level];
+    Level& C = ctx->parts[0].lev[level + 1];
     Stage sc, sx;
-    if ((rc = stage_in(ctx, sc, xc, nodes_of(C.L), st)) || (rc = stage_in(ctx, sx, x, nodes_of(F.L), st)))
-        return rc;
-    launch_nat2int(C.L, sc.d, C.lam, true, st);
-    launch_nat2int(F.L, sx.d, F.lam, true, st);
+    RC(stage_in(ctx, sc, xc, nodes_of(C.L), st));
+    RC(stage_in(ctx, sx, x, nodes_of(F.L), st));
+    launch_nat2int(C.L, whole(C.L, sc.d), C.lam, true, st);
+    launch_nat2int(F.L, whole(F.L, sx.d), F.lam, true, st);
     launch_prolong(F.L, C.L, F.M, C.lam, F.lam, st);
     sx.out = true;
     sx.host = x;
-    launch_int2nat(F.L, F.lam, sx.d, st);
+    launch_int2nat(F.L, F.lam, whole(F.L, sx.d), st);
     CKL();
     return stage_finish(st, {&sc, &sx});
 }
 
 int wd_coarse_solve(wd_ctx* ctx, const double* f, double* x, void* stream) {
     if (!ctx || !f || !x) return fail(WD_E_INVAL, "NULL argument");
+    RC(check_single(ctx));
     cudaStream_t st = (cudaStream_t)stream;
-    Level& lc = ctx->lev[ctx->nlev - 1];
+    Level& lc = ctx->parts[0].lev[ctx->nlev - 1];
     const size_t N = nodes_of(lc.L);
     Stage sf, sx;
-    int rc;
-    if ((rc = stage_in(ctx, sf, f, N, st)) || (rc = stage_out(ctx, sx, x, N))) return rc;
-    launch_nat2int(lc.L, sf.d, lc.f, true, st);
+    RC(stage_in(ctx, sf, f, N, st));
+    RC(stage_out(ctx, sx, x, N));
+    launch_nat2int(lc.L, whole(lc.L, sf.d), lc.f, true, st);
     CK(cudaMemsetAsync(lc.lam, 0, sizeof(double) * lc.L.NT, st));
-    if ((rc = coarse_solve(ctx, st))) return rc;
-    launch_int2nat(lc.L, lc.lam, sx.d, st);
+    RC(coarse_solve(ctx, st));
+    launch_int2nat(lc.L, lc.lam, whole(lc.L, sx.d), st);
     CKL();
     return stage_finish(st, {&sf, &sx});
 }
@@ -1008,17 +1533,17 @@ int wd_residual_norm(wd_ctx* ctx, const double* x, const double* f, double* abs_
                      double* rel_out, void* stream) {
     if (!ctx || !x || !f) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
-    Level& F = ctx->lev[0];
-    const size_t N = nodes_of(F.L);
     Stage sx, sf;
-    int rc;
-    if ((rc = stage_in(ctx, sx, x, N, st)) || (rc = stage_in(ctx, sf, f, N, st))) return rc;
-    launch_nat2int(F.L, sx.d, F.lam, true, st);
-    launch_nat2int(F.L, sf.d, F.f, true, st);
+    RC(stage_in(ctx, sx, x, abi_nodes(ctx), st));
+    RC(stage_in(ctx, sf, f, abi_nodes(ctx), st));
+    for (Part& P : ctx->parts) {
+        launch_nat2int(P.lev[0].L, nat_nodes(ctx, P, sx.d), P.lev[0].lam, true, st);
+        launch_nat2int(P.lev[0].L, nat_nodes(ctx, P, sf.d), P.lev[0].f, true, st);
+    }
     CKL();
-    if ((rc = residual_sq(ctx, 0, st)) || (rc = norm_sq(ctx, F.L, F.f, 1, st)) ||
-        (rc = fetch_scalars(ctx, 2, st)))
-        return rc;
+    RC(residual_sq(ctx, 0, st));
+    RC(norm_sq(ctx, ARR_F, 1, st));
+    RC(fetch_scalars(ctx, 2, st));
     const double a = std::sqrt(ctx->hscal[0]), fn = std::sqrt(ctx->hscal[1]);
     if (abs_out) *abs_out = a;
     if (rel_out) *rel_out = fn > 0 ? a / fn : a;

@@ -30,11 +30,36 @@ typedef long long i64;
 
 // Row-outer layout [j][k][half][pos]: one node row of all levels (n3 * P
 // doubles) is contiguous, so a slab halo row is a single block to copy/send.
+//
+// Slab decomposition: a level may hold only the node rows
+// [jg0, jg0 + n2) of a grid with n2g rows (its own rows plus halo rows).
+// Kernels update only the owned local rows [own0, own1); the Dirichlet set is
+// decided on global rows (jg = j + jg0 in {0, n2g - 1}).  Without
+// decomposition jg0 = 0, n2g = n2, own0 = 0, own1 = n2.
 struct LevDev {
     int n1, n2, n3;
     int H, P;      // half-row pitch, row pitch (2H)
     i64 sk, sj;    // strides of k (= P) and of j (= n3 P)
     i64 NT;        // entries per array (= n2 sj)
+    int jg0, n2g;  // global row of local row 0, global row count
+    int own0, own1;  // owned local rows
+};
+
+// node row j (local) is owned and not a lateral Dirichlet row
+__host__ __device__ __forceinline__ bool row_free(const LevDev& L, int j) {
+    const int g = j + L.jg0;
+    return j >= L.own0 && j < L.own1 && g >= 1 && g <= L.n2g - 2;
+}
+__host__ __device__ __forceinline__ bool row_dirichlet(const LevDev& L, int j) {
+    const int g = j + L.jg0;
+    return g == 0 || g == L.n2g - 1;
+}
+
+// a natural-layout array of the ABI: node (i, j_loc, k) at
+// (k * n2a + j_loc + jofs) * n1 + i   (element arrays: rows n2a, columns n1).
+struct Nat {
+    const double* p;
+    int n2a, jofs;
 };
 
 __host__ __device__ __forceinline__ i64 loff(const LevDev& L, int i, int j, int k) {
@@ -68,18 +93,19 @@ __host__ __device__ __forceinline__ int slot_of(int dx, int dy, int dz) {
 void launch_assemble(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
                      const double c[3], const LevDev& L, double* coef,
                      unsigned long long* bad, cudaStream_t st);
-void launch_rhs(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
-                const double* u0, double* f, cudaStream_t st);
-void launch_recover(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
-                    const double c[3], const double* lam, const double* u0, double* u,
-                    cudaStream_t st);
+void launch_rhs(const double* X, const double* Y, const double* Z, const LevDev& L, Nat u0, Nat f,
+                cudaStream_t st);
+void launch_recover(const double* X, const double* Y, const double* Z, const LevDev& L,
+                    const double c[3], Nat lam, Nat u0, Nat u, cudaStream_t st);
 
 // k_mg.cu: multigrid on the stencil
-void launch_nat2int(const LevDev& L, const double* src, double* dst, bool zero_dirichlet,
-                    cudaStream_t st);
-void launch_int2nat(const LevDev& L, const double* src, double* dst, cudaStream_t st);
+void launch_nat2int(const LevDev& L, Nat src, double* dst, bool zero_dirichlet, cudaStream_t st);
+void launch_int2nat(const LevDev& L, const double* src, Nat dst, cudaStream_t st);
 void launch_gs_sweep(const LevDev& L, const double* coef, double* lam, const double* f,
                      cudaStream_t st);
+void launch_gs_phase(const LevDev& L, const double* coef, double* lam, const double* f, int c,
+                     cudaStream_t st);
+void launch_sum_ordered(const double* v, int n, double* out, cudaStream_t st);
 // y = K x (f == NULL) or y = f - K x; optional block partials of sum y^2
 int launch_apply(const LevDev& L, const double* coef, const double* x, const double* f,
                  double* y, double* partial, cudaStream_t st);
