@@ -16,8 +16,8 @@ with host buffers, clocks and the launch count.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config paper|medium|small|tiny]
-Under torchrun (N > 1) every rank solves its own copy of the workload
-(independent problems, no data-path collective: "scaling": "weak").
+Under torchrun (N > 1) the one grid is split into N slabs of node rows (one
+per GPU, halo rows and coarse levels over NCCL): "scaling": "strong".
 """
 from __future__ import annotations
 
@@ -194,13 +194,13 @@ def run_reference(args, ws, rank):
 
 
 # ---------------------------------------------------------------- GPU arm
-def gpu_step(wd, prob, opt, tol, stream, host=None):
+def gpu_step(wd, prob, opt, tol, stream, host=None, n2g=None):
     """One full step through the C ABI.  host: dict of pinned host tensors for
     the end-to-end variant (inputs copied in, lambda and u copied out)."""
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     ev[0].record(stream)
     if host is None:
-        ctx = wd.wd_assemble(prob.X, prob.Y, prob.Z, prob.a, opt)
+        ctx = wd.wd_assemble(prob.X, prob.Y, prob.Z, prob.a, opt, n2_global=n2g)
         ev[1].record(stream)
         f = wd.wd_rhs(ctx, prob.u0)
         ev[2].record(stream)
@@ -208,7 +208,7 @@ def gpu_step(wd, prob, opt, tol, stream, host=None):
         ev[3].record(stream)
         u = wd.wd_recover_wind(ctx, lam, prob.u0)
     else:
-        ctx = wd.wd_assemble(host["X"], host["Y"], host["Z"], prob.a, opt)
+        ctx = wd.wd_assemble(host["X"], host["Y"], host["Z"], prob.a, opt, n2_global=n2g)
         ev[1].record(stream)
         f = torch.empty(ctx.node_shape, dtype=torch.float64, device="cuda")
         wd.wd_rhs(ctx, host["u0"], f)
@@ -225,12 +225,30 @@ def run_ours(args, ws, rank, local):
     import paper_2101_08453_b200 as wd
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    prob = make_problem(args.config, dev)
-    opt = wd.default_options(profile=1, coarsen_rule=args.rule)
-    nodes = prob.n_nodes
+    full = make_problem(args.config, dev)
+    nodes = full.n_nodes
+    n2 = full.dims[1]
+    if ws > 1:
+        # slab decomposition of the one grid: this rank keeps its
+        # node rows + 2 halo rows; halos and coarse levels move over NCCL
+        import synth
+        comm = wd.nccl_comm_from_torch()
+        jb, je = wd.wd_partition_rows(n2, ws, rank)
+        lo, hi = wd.slab_rows(n2, ws, rank)
+        prob = synth.Problem(full.name, full.nx, hi - lo - 1, full.nz,
+                             full.X[:, lo:hi].contiguous(), full.Y[:, lo:hi].contiguous(),
+                             full.Z[:, lo:hi].contiguous(),
+                             full.u0[:, :, lo:hi - 1].contiguous(), full.a, dict(full.meta))
+        del full
+        opt = wd.default_options(profile=1, coarsen_rule=args.rule, nranks=ws, rank=rank,
+                                 nccl_comm=comm, j_begin=jb, j_end=je)
+    else:
+        prob = full
+        opt = wd.default_options(profile=1, coarsen_rule=args.rule)
+    scaling = "strong" if ws > 1 else "weak"
 
     def one(host=None):
-        ctx, ev, rep, prof, keep = gpu_step(wd, prob, opt, args.tol, stream, host)
+        ctx, ev, rep, prof, keep = gpu_step(wd, prob, opt, args.tol, stream, host, n2)
         return ctx, ev, rep, prof
 
     def hier_info(ctx):
@@ -271,12 +289,15 @@ def run_ours(args, ws, rank, local):
     barrier(ws)
     ms_total = max_over_ranks(ws, start.elapsed_time(stop))
     ms_step = ms_total / args.steps
-    value = ws * nodes * (cycles / args.steps) / (ms_step * 1e-3)
+    value = nodes * (cycles / args.steps) / (ms_step * 1e-3)   # one global grid on ws GPUs
 
     # roofline of the dominant kernel: one colour phase of the level-0 smoother
     peak, peak_src = measured_hbm_peak()
-    n1, n2, n3 = prob.dims
-    free0 = (n1 - 2) * (n2 - 2) * (n3 - 1)
+    n1, _, n3 = prob.dims
+    if ws > 1:   # this rank's free rows
+        free0 = (n1 - 2) * (min(je, n2 - 1) - max(jb, 1)) * (n3 - 1)
+    else:
+        free0 = (n1 - 2) * (n2 - 2) * (n3 - 1)
     launch_ms = gs_ms / max(gs_sweeps, 1) / 4.0
     bytes_launch = GS_BYTES_PER_FREE_NODE_PER_LAUNCH * free0
     achieved = bytes_launch / (launch_ms * 1e-3) / 1e9 if launch_ms > 0 else 0.0
@@ -293,7 +314,7 @@ def run_ours(args, ws, rank, local):
         line = {
             "metric": "fine node-V-cycles/s", "value": value, "unit": "node-cycles/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": CONFIG_NAMES[args.config], "nodes": nodes,
                        "elements": prob.nx * prob.ny * prob.nz, "free_unknowns": free0,
@@ -301,7 +322,7 @@ def run_ours(args, ws, rank, local):
                        "levels": levels, "plans_horizontal": [p["horizontal"] for p in plans],
                        "step": "wd_assemble + wd_rhs + wd_solve(zero start) + wd_recover_wind",
                        "l2": "inputs larger than L2 (no flush)",
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+                       "parallelism": f"slabs x{ws} (NCCL)" if ws > 1 else "1 GPU"},
             "cycles_per_step": cycles / args.steps, "rate": float(np.mean(rates)),
             "time_to_1e-8_s": parts[2] / args.steps * 1e-3,
             "breakdown_ms": {"assemble_setup": parts[0] / args.steps,
@@ -338,10 +359,10 @@ def run_ours(args, ws, rank, local):
         s1.record(stream)
         torch.cuda.synchronize()
         ems = max_over_ranks(ws, s0.elapsed_time(s1)) / ne
-        nb = 8 * nodes
-        ne_el = 8 * prob.nx * prob.ny * prob.nz * 3
+        nb = 8 * prob.X.numel() * ws                     # whole job (slabs incl. halo rows)
+        ne_el = 8 * prob.u0.numel() * ws
         if line is not None:
-            line["e2e"] = {"value": ws * nodes * (ecyc / ne) / (ems * 1e-3),
+            line["e2e"] = {"value": nodes * (ecyc / ne) / (ems * 1e-3),
                            "unit": "node-cycles/s", "ms_per_step": ems,
                            "h2d_bytes_per_step": 3 * nb + 2 * ne_el + nb,
                            "d2h_bytes_per_step": nb + ne_el,

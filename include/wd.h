@@ -105,7 +105,8 @@ typedef struct {
 void wd_default_options(wd_options* opt);
 
 /* Setup once per mesh (P:107-111 assembly, P:151-158 + P:192-202 hierarchy).
- * X, Y, Z: node coordinates [n3][n2][n1]; a1, a2, a3 > 0: penalty constants of
+ * X, Y, Z: node coordinates [n3][n2][n1] (in NCCL mode [n3][slab rows][n1],
+ * n2 still being the grid's row count); a1, a2, a3 > 0: penalty constants of
  * A = diag(a1^2, a2^2, a3^2).  Validates the mesh (WD_E_MESH names
  * the lowest failing element), assembles the 27-point operator (stored as 14
  * symmetric coefficients per node), plans the coarsening, forms the Galerkin

@@ -147,10 +147,11 @@ def default_options(**kw) -> wd_options:
 class Context:
     """Owns a ``wd_ctx*`` (hierarchy and workspaces on the device)."""
 
-    def __init__(self, handle, dims, device):
+    def __init__(self, handle, dims, device, rows=None):
         self.h = handle
-        self.dims = dims        # (n1, n2, n3)
+        self.dims = dims        # global node dims (n1, n2, n3)
         self.device = device
+        self.rows = rows if rows is not None else dims[1]   # node rows of the ABI arrays
 
     def __del__(self):
         self.close()
@@ -162,13 +163,14 @@ class Context:
 
     @property
     def node_shape(self):
-        n1, n2, n3 = self.dims
-        return (n3, n2, n1)
+        """Shape of the node arrays of the ABI calls (a slab in NCCL mode)."""
+        n1, _, n3 = self.dims
+        return (n3, self.rows, n1)
 
     @property
     def elem_shape(self):
-        n1, n2, n3 = self.dims
-        return (3, n3 - 1, n2 - 1, n1 - 1)
+        n1, _, n3 = self.dims
+        return (3, n3 - 1, self.rows - 1, n1 - 1)
 
     def device_bytes(self):
         return int(_lib.wd_device_bytes(self.h))
@@ -255,13 +257,16 @@ def wd_gather_level(ctx: "Context") -> int:
 
 
 # ------------------------------------------------------------------ ABI calls
-def wd_assemble(X, Y, Z, a, opt: wd_options | None = None) -> Context:
-    n3, n2, n1 = X.shape
+def wd_assemble(X, Y, Z, a, opt: wd_options | None = None, n2_global=None) -> Context:
+    """X, Y, Z: node arrays (n3, rows, n1); rows = n2 except in NCCL mode, where
+    they hold this rank's slab (slab_rows) and n2_global gives the grid's n2."""
+    n3, rows, n1 = X.shape
+    n2 = int(n2_global) if n2_global is not None else rows
     h = C.c_void_p()
     o = opt if opt is not None else default_options()
     _check(_lib.wd_assemble(_ptr(X), _ptr(Y), _ptr(Z), n1, n2, n3, float(a[0]), float(a[1]),
                             float(a[2]), C.byref(o), _stream(X), C.byref(h)))
-    return Context(h, (n1, n2, n3), X.device)
+    return Context(h, (n1, n2, n3), X.device, rows)
 
 
 def wd_rhs(ctx: Context, u0, f=None):
