@@ -43,7 +43,7 @@ constexpr int F_ELEMS = pad128(TJ * 2 * TI);
 constexpr int B_ELEMS = pad128(9 * B_ROWS * 2 * BP);
 constexpr int X_ELEMS = pad128(X_ROWS * 2 * BP);
 constexpr size_t SMEM = (size_t)8 * (RA * (A_ELEMS + F_ELEMS) + RB * B_ELEMS + RX * X_ELEMS) +
-                        8 * (RA + RB + RX) + 8 * 8 + 256;
+                        2 * 8 * (RA + RB + RX) + 8 * 8 + 256;
 
 __device__ __forceinline__ uint32_t sa(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -113,19 +113,14 @@ __device__ __forceinline__ void load_X(const CUtensorMap* mX, double* x, uint64_
     if (!(dbg & 4)) tma4(x, mX, a0 > 0 ? a0 - 2 : 0, 0, j0 > 0 ? j0 - 1 : 0, k, bar);
 }
 
-__device__ __forceinline__ double block_sum256(double v, double* ws) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    const int t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-    if ((t & 31) == 0) ws[t >> 5] = v;
-    __syncthreads();
-    double r = 0.0;
-    if (t == 0)
-        for (int w = 0; w < NTHR / 32; w++) r += ws[w];
-    return r;
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
 }
 
-__global__ void __launch_bounds__(NTHR, 1)
+// Warp-specialised: warps 0..7 compute (one node column each), warp 8 is the
+// TMA producer.  full[] barriers complete when a unit's bytes have landed;
+// empty[] barriers (8 arrivals, one per consumer warp) release a slot.
+__global__ void __launch_bounds__(NTHR + 32, 1)
 apply_tma_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
                  const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mF,
                  LevDev L, Tiles T, int with_f, int dbg, double* __restrict__ y,
@@ -136,53 +131,59 @@ apply_tma_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__
     double* sF = sA + RA * A_ELEMS;
     double* sB = sF + RA * F_ELEMS;
     double* sX = sB + RB * B_ELEMS;
-    uint64_t* bA = reinterpret_cast<uint64_t*>(sX + RX * X_ELEMS);
-    uint64_t* bB = bA + RA;
-    uint64_t* bX = bB + RB;
-    double* ws = reinterpret_cast<double*>(bX + RX);
+    uint64_t* fA = reinterpret_cast<uint64_t*>(sX + RX * X_ELEMS);
+    uint64_t* fB = fA + RA;
+    uint64_t* fX = fB + RB;
+    uint64_t* eA = fX + RX;
+    uint64_t* eB = eA + RA;
+    uint64_t* eX = eB + RB;
+    double* ws = reinterpret_cast<double*>(eX + RX);
 
-    const int tx = threadIdx.x, ci = threadIdx.y, tz = threadIdx.z;
-    const bool leader = tx == 0 && ci == 0 && tz == 0;
-    if (leader) {
-        for (int t = 0; t < RA; t++) mbar_init(&bA[t], 1);
-        for (int t = 0; t < RB; t++) mbar_init(&bB[t], 1);
-        for (int t = 0; t < RX; t++) mbar_init(&bX[t], 1);
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    constexpr int NCW = NTHR / 32;   // consumer warps
+    if (tid == 0) {
+        for (int t = 0; t < RA; t++) { mbar_init(&fA[t], 1); mbar_init(&eA[t], NCW); }
+        for (int t = 0; t < RB; t++) { mbar_init(&fB[t], 1); mbar_init(&eB[t], NCW); }
+        for (int t = 0; t < RX; t++) { mbar_init(&fX[t], 1); mbar_init(&eX[t], NCW); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     const int nk = T.nk;                  // levels per tile: 0 .. n3-2
     const int my_tiles = (T.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int nsteps = my_tiles * nk;     // AB units = steps; X units = my_tiles * (nk + 1)
+    const int nsteps = my_tiles * nk;
     auto tile_of = [&](int it, int& a0, int& j0) {
         const int t = (int)blockIdx.x + it * (int)gridDim.x;
         a0 = (t % T.ntx) * TI;
         j0 = L.own0 + (t / T.ntx) * TJ;   // tiles cover the owned local rows
     };
-    // producer state: next AB step and next X unit to issue
-    int pAB = 0, pX = 0;
-    auto produce = [&](int upto_step) {
-        // AB units up to step `upto_step`, X units up to the level k+1 of that step
-        while (pAB <= upto_step && pAB < nsteps) {
-            int a0, j0;
-            tile_of(pAB / nk, a0, j0);
-            const int k = pAB % nk;
-            load_AB(&mA, &mB, &mF, sA + (pAB % RA) * A_ELEMS, sF + (pAB % RA) * F_ELEMS,
-                    sB + (pAB % RB) * B_ELEMS, &bA[pAB % RA], &bB[pAB % RB], a0, j0, k,
-                    with_f != 0, dbg);
-            pAB++;
-        }
-        const int last = upto_step < nsteps ? upto_step : nsteps - 1;
-        const int xneed = (last / nk) * (nk + 1) + (last % nk) + 1;   // X unit of level k+1
-        while (pX <= xneed && pX < my_tiles * (nk + 1)) {
-            int a0, j0;
-            tile_of(pX / (nk + 1), a0, j0);
-            load_X(&mX, sX + (pX % RX) * X_ELEMS, &bX[pX % RX], a0, j0, pX % (nk + 1), dbg);
-            pX++;
-        }
-    };
-    if (leader && nsteps > 0) produce(D - 1);
 
+    if (warp == NCW) {
+        // ---------------- producer: units in consumption order, gated by empty[]
+        if (lane == 0) {
+            for (int s = 0; s < nsteps; s++) {
+                const int it = s / nk, k = s % nk;
+                int a0, j0;
+                tile_of(it, a0, j0);
+                mbar_wait(&eA[s % RA], ((s / RA) & 1) ^ 1);
+                mbar_wait(&eB[s % RB], ((s / RB) & 1) ^ 1);
+                load_AB(&mA, &mB, &mF, sA + (s % RA) * A_ELEMS, sF + (s % RA) * F_ELEMS,
+                        sB + (s % RB) * B_ELEMS, &fA[s % RA], &fB[s % RB], a0, j0, k, with_f != 0,
+                        dbg);
+                const int xu = it * (nk + 1) + k;
+                for (int u = (k == 0 ? xu : xu + 1); u <= xu + 1; u++) {
+                    mbar_wait(&eX[u % RX], ((u / RX) & 1) ^ 1);
+                    load_X(&mX, sX + (u % RX) * X_ELEMS, &fX[u % RX], a0, j0, u - it * (nk + 1), dbg);
+                }
+            }
+        }
+        __syncthreads();
+        return;
+    }
+
+    // ---------------- consumers
+    const int tx = lane, ci = warp & 1, tz = warp >> 1;
     const int hp = 1 - ci;
     double acc = 0.0;
     double xm[9], x0[9], xp[9];
@@ -191,12 +192,11 @@ apply_tma_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__
         const int it = s / nk, k = s % nk;
         int a0, j0;
         tile_of(it, a0, j0);
-        if (leader) produce(s + D);
         const int xu = it * (nk + 1) + k;         // X unit of level k
-        mbar_wait(&bA[s % RA], (s / RA) & 1);
-        mbar_wait(&bB[s % RB], (s / RB) & 1);
-        mbar_wait(&bX[(xu + 1) % RX], ((xu + 1) / RX) & 1);
-        if (k == 0) mbar_wait(&bX[xu % RX], (xu / RX) & 1);
+        mbar_wait(&fA[s % RA], (s / RA) & 1);
+        mbar_wait(&fB[s % RB], (s / RB) & 1);
+        mbar_wait(&fX[(xu + 1) % RX], ((xu + 1) / RX) & 1);
+        if (k == 0) mbar_wait(&fX[xu % RX], (xu / RX) & 1);
         const double* A = sA + (s % RA) * A_ELEMS;
         const double* Fb = sF + (s % RA) * F_ELEMS;
         const double* B = sB + (s % RB) * B_ELEMS;
@@ -235,7 +235,8 @@ apply_tma_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__
             auto b_at = [&](const double* Bx, int sl, int r, int h, int q) {
                 return Bx[(((sl - 5) * B_ROWS + r) * 2 + h) * BP + q];
             };
-            double s_ = a_at(0, rr, ci, p) * x0[4];
+            // four independent partial sums (ILP), combined in a fixed order
+            double s0 = a_at(0, rr, ci, p) * x0[4], s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
             for (int sl = 1; sl < 14; sl++) {
                 const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
@@ -244,13 +245,14 @@ apply_tma_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__
                 const int hb = dx ? hp : ci;
                 const int qb = dx > 0 ? pm : (dx < 0 ? pp : p);   // position of i - dx
                 if (!dz) {
-                    s_ = fma(a_at(sl, rr, ci, p), x0[cf], s_);
-                    s_ = fma(a_at(sl, rr - dy, hb, qb), x0[cb], s_);
+                    s0 = fma(a_at(sl, rr, ci, p), x0[cf], s0);
+                    s1 = fma(a_at(sl, rr - dy, hb, qb), x0[cb], s1);
                 } else {
-                    s_ = fma(b_at(B, sl, rr, ci, p), xp[cf], s_);
-                    if (k > 0) s_ = fma(b_at(Bm, sl, rr - dy, hb, qb), xm[cb], s_);
+                    s2 = fma(b_at(B, sl, rr, ci, p), xp[cf], s2);
+                    if (k > 0) s3 = fma(b_at(Bm, sl, rr - dy, hb, qb), xm[cb], s3);
                 }
             }
+            const double s_ = (s0 + s1) + (s2 + s3);
             const double v = with_f ? Fb[(tz * 2 + ci) * TI + tx] - s_ : s_;
             y[loff(L, i, j, k)] = v;
             acc = fma(v, v, acc);
@@ -260,11 +262,28 @@ apply_tma_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__
             xm[c] = x0[c];
             x0[c] = xp[c];
         }
-        __syncthreads();   // all consumers done with this step's slots
+        // release this step's slots (B of level k-1 now, B of level k after
+        // the next level, or now at the tile's last level)
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&eA[s % RA]);
+            mbar_arrive(&eX[(xu + 1) % RX]);
+            if (k == 0) mbar_arrive(&eX[xu % RX]);
+            if (k > 0) mbar_arrive(&eB[(s + RB - 1) % RB]);
+            if (k == nk - 1) mbar_arrive(&eB[s % RB]);
+        }
     }
+    __syncthreads();
     if (partial) {
-        const double sum = block_sum256(acc, ws);
-        if (leader) partial[blockIdx.x] = sum;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if (lane == 0) ws[warp] = acc;
+        asm volatile("bar.sync 1, %0;" ::"n"(NTHR));   // consumer warps only
+        if (tid == 0) {
+            double r = 0.0;
+            for (int w = 0; w < NCW; w++) r += ws[w];
+            partial[blockIdx.x] = r;
+        }
     }
 }
 
@@ -348,7 +367,7 @@ int launch_apply_tma(const LevDev& L, const void* mapA, const void* mapB, const 
     if (g > T.ntiles) g = T.ntiles;
     const CUtensorMap* F = (const CUtensorMap*)(mapF ? mapF : mapX);
     g_launches += 1;
-    apply_tma_kernel<<<g, dim3(TI, 2, TJ), SMEM, st>>>(
+    apply_tma_kernel<<<g, NTHR + 32, SMEM, st>>>(
         *(const CUtensorMap*)mapA, *(const CUtensorMap*)mapB, *(const CUtensorMap*)mapX, *F, L, T,
         mapF ? 1 : 0, g_tma_debug, y, partial);
     return g;
