@@ -368,6 +368,39 @@ def run_ours(args, ws, rank, local):
                            "d2h_bytes_per_step": nb + ne_el,
                            "note": "pinned host X,Y,Z,u0 in; lambda,u out; copies inside the ABI calls"}
         del host
+    # BASELINE configs[4]: warm-start sequence on the same grid: u0_s =
+    # u0_{s-1} + smooth increment (seeds 4..13); each step wd_rhs + wd_solve from
+    # lambda_{s-1} + wd_recover_wind, hierarchy reused (same mesh and A)
+    if args.warm > 0 and ws == 1:
+        import synth
+        ctx = wd.wd_assemble(prob.X, prob.Y, prob.Z, prob.a, opt, n2_global=n2)
+        lam = torch.zeros(ctx.node_shape, dtype=torch.float64, device=dev)
+        f = wd.wd_rhs(ctx, prob.u0)
+        lam, rep0 = wd.wd_solve(ctx, f, rel_tol=args.tol, raise_on_noconv=False)
+        incs = [synth.warm_increment(prob, 4 + s) for s in range(args.warm)]
+        u0 = prob.u0.clone()
+        cyc, rel0 = [], []
+        torch.cuda.synchronize()
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        for s in range(args.warm):
+            u0 += incs[s]
+            f = wd.wd_rhs(ctx, u0, f)
+            lam, rp = wd.wd_solve(ctx, f, lam0=lam, rel_tol=args.tol, lam=lam,
+                                  raise_on_noconv=False)
+            u = wd.wd_recover_wind(ctx, lam, u0)
+            cyc.append(rp["cycles"])
+            rel0.append(rp["rel_res0"])
+        w1.record(stream)
+        torch.cuda.synchronize()
+        if line is not None:
+            line["warm_start"] = {
+                "config": "BASELINE configs[4] on 1 GPU: paper grid, 10 steps, seeds 4..13",
+                "steps": args.warm, "cycles_per_step": cyc, "initial_rel_res": rel0,
+                "cold_start_cycles": rep0["cycles"],
+                "ms_per_step": w0.elapsed_time(w1) / args.warm,
+                "step": "wd_rhs + wd_solve(lambda_{s-1}) + wd_recover_wind (hierarchy reused)"}
+        del ctx, u
     # oracle baseline on the host cores (rank 0, N = 1 only)
     if rank == 0 and ws == 1 and not args.no_cpu:
         import oracle
@@ -399,6 +432,7 @@ def main():
                     choices=["coupling_cur", "coupling_paper", "verbatim", "full"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--warm", type=int, default=10, help="warm-start steps (configs[4]); 0 = off")
     args = ap.parse_args()
     ws, rank, local = dist_setup()
     if args.impl == "reference":

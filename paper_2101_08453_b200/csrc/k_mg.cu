@@ -250,6 +250,7 @@ restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
     double wx[3], wy[3];
     const int mx = support1d(M.pos[0], M.co[0], F.n1, I, tx, wx);
     const int my = support1d(M.pos[1], M.co[1], F.n2, J, ty, wy);
+#pragma unroll 4
     for (int Kc = 0; Kc <= C.n3 - 2; Kc++) {
         int tz[3];
         double wz[3];
@@ -266,13 +267,15 @@ restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
 }
 
 __global__ void __launch_bounds__(128)
-prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc, double* x) {
+prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
+               double* __restrict__ x) {
     const int i = blockIdx.x * 128 + threadIdx.x;
     const int j = blockIdx.y;
     if (i < 1 || i > F.n1 - 2 || !row_free(F, j)) return;
     const int ix = M.lo[0][i], iy = M.lo[1][j];
     const int nx = M.co[0][i] ? 1 : 2, ny = M.co[1][j] ? 1 : 2;
     const double wx = nx == 1 ? 1.0 : 0.5, wy = ny == 1 ? 1.0 : 0.5;
+#pragma unroll 4
     for (int k = 0; k <= F.n3 - 2; k++) {
         const int iz = M.lo[2][k];
         const int nz = M.co[2][k] ? 1 : 2;
