@@ -38,7 +38,10 @@ sys.path.insert(0, ROOT)
 CONFIG_NAMES = {"tiny": "tiny 16x16x8 (configs[0])", "small": "small 128x128x10 (configs[1])",
                 "medium": "medium 1000x1000x15 (configs[2])",
                 "paper": "paper-scale 3000x3000x15 (configs[3])"}
-GS_BYTES_PER_FREE_NODE_PER_LAUNCH = 66   # 264 B/node/sweep over 4 phases
+# algorithmic HBM bytes per free node of one launch of the level-0 smoother:
+#   fused sweep (1 launch/sweep): 14 stored couplings (112) + f (8) + lambda read + write (16)
+#   colour phase (4 launches/sweep, slab levels): 264 B/node/sweep / 4
+GS_BYTES = {"fused": (136, 1, "gs_fused_kernel"), "phased": (66, 4, "gs_phase_kernel")}
 CPU_CROP = 200                            # oracle sample: 200x200x15 elements of the workload
 
 
@@ -240,11 +243,11 @@ def run_ours(args, ws, rank, local):
                              full.Z[:, lo:hi].contiguous(),
                              full.u0[:, :, lo:hi - 1].contiguous(), full.a, dict(full.meta))
         del full
-        opt = wd.default_options(profile=1, coarsen_rule=args.rule, nranks=ws, rank=rank,
+        opt = wd.default_options(profile=1, coarsen_rule=args.rule, smoother=args.smoother, nranks=ws, rank=rank,
                                  nccl_comm=comm, j_begin=jb, j_end=je)
     else:
         prob = full
-        opt = wd.default_options(profile=1, coarsen_rule=args.rule)
+        opt = wd.default_options(profile=1, coarsen_rule=args.rule, smoother=args.smoother)
     scaling = "strong" if ws > 1 else "weak"
 
     def one(host=None):
@@ -291,21 +294,24 @@ def run_ours(args, ws, rank, local):
     ms_step = ms_total / args.steps
     value = nodes * (cycles / args.steps) / (ms_step * 1e-3)   # one global grid on ws GPUs
 
-    # roofline of the dominant kernel: one colour phase of the level-0 smoother
+    # roofline of the dominant kernel: the level-0 smoother launch (one fused sweep;
+    # one colour phase on slab levels, which always use the phased schedule)
     peak, peak_src = measured_hbm_peak()
     n1, _, n3 = prob.dims
     if ws > 1:   # this rank's free rows
         free0 = (n1 - 2) * (min(je, n2 - 1) - max(jb, 1)) * (n3 - 1)
     else:
         free0 = (n1 - 2) * (n2 - 2) * (n3 - 1)
-    launch_ms = gs_ms / max(gs_sweeps, 1) / 4.0
-    bytes_launch = GS_BYTES_PER_FREE_NODE_PER_LAUNCH * free0
+    gs_kind = "fused" if (args.smoother == "fused" and ws == 1) else "phased"
+    gs_b, gs_per_sweep, gs_name = GS_BYTES[gs_kind]
+    launch_ms = gs_ms / max(gs_sweeps, 1) / gs_per_sweep
+    bytes_launch = gs_b * free0
     achieved = bytes_launch / (launch_ms * 1e-3) / 1e9 if launch_ms > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_gs_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config)
+            traffic = json.load(open(tp)).get(f"{gs_name}:{args.config}")
         except Exception:
             traffic = None
 
@@ -330,7 +336,7 @@ def run_ours(args, ws, rank, local):
                              "recover": parts[3] / args.steps},
             "ms_per_vcycle": vc_ms / max(vc_n, 1),
             "device_bytes": dev_bytes,
-            "roofline": {"kernel": "gs_phase_kernel (level 0)", "bound": "hbm",
+            "roofline": {"kernel": f"{gs_name} (level 0)", "bound": "hbm",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "bytes_per_launch": bytes_launch, "launch_ms": launch_ms,
@@ -430,6 +436,7 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--rule", default="coupling_cur",
                     choices=["coupling_cur", "coupling_paper", "verbatim", "full"])
+    ap.add_argument("--smoother", default="fused", choices=["fused", "phased"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--warm", type=int, default=10, help="warm-start steps (configs[4]); 0 = off")

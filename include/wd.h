@@ -60,6 +60,15 @@ enum {
  *  FULL           base method: 2x2x2 coarsening at every level */
 enum { WD_RULE_COUPLING_CUR = 0, WD_RULE_COUPLING_PAPER = 1, WD_RULE_VERBATIM = 2, WD_RULE_FULL = 3 };
 
+/* Schedule of the 4-colour smoother.  Both compute the same
+ * iterate bit for bit (same operations in the same order per node):
+ *  FUSED   one launch per sweep: all four colour phases pipelined over k in
+ *          shared-memory tiles (k_gs_fused.cu); used on every level that is
+ *          not split into slabs (default)
+ *  PHASED  four launches per sweep, one per colour (k_mg.cu gs_phase_kernel);
+ *          always used on slab levels */
+enum { WD_SMOOTH_FUSED = 0, WD_SMOOTH_PHASED = 1 };
+
 typedef struct wd_ctx wd_ctx;
 
 typedef struct {
@@ -85,6 +94,7 @@ typedef struct {
     int j_begin, j_end;      /* owned node rows [j_begin, j_end) of this rank; must equal
                                 wd_partition_rows(n2, nranks, rank) */
     int profile;             /* 1: CUDA events around level-0 smoothing and each V-cycle (default 0) */
+    int smoother;            /* WD_SMOOTH_* (default WD_SMOOTH_FUSED) */
 } wd_options;
 
 typedef struct {
@@ -202,9 +212,10 @@ void wd_profile_reset(wd_ctx* ctx);
  * process (a CUDA-graph replay counts its kernel nodes). */
 long long wd_launch_count(void);
 /* Time one internal kernel (or step) on the context's own buffers with CUDA
- * events: which = 0 GS sweep (4 colour phases), 1 residual apply, 2 restrict
- * (level -> level+1), 3 prolong, 4 V-cycle (level 0), 5 residual norm
- * (level 0), 6 Galerkin (level -> level+1), 7 level-0 assembly.  One untimed
+ * events: which = 0 GS sweep (the context's smoother), 1 residual apply,
+ * 2 restrict (level -> level+1), 3 prolong, 4 V-cycle (level 0), 5 residual
+ * norm (level 0), 6 Galerkin (level -> level+1), 7 level-0 assembly, 8 GS
+ * sweep as 4 colour-phase launches.  One untimed
  * warm-up, then *ms_out = mean over `reps`.  Overwrites internal vectors
  * (and, for 6/7, recomputes identical operators). */
 int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out);

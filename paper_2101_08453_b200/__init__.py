@@ -27,6 +27,7 @@ _lib = C.CDLL(LIB_PATH)
 WD_OK, WD_E_INVAL, WD_E_MESH, WD_E_NOCONV, WD_E_DIVERGED, WD_E_NONFINITE, WD_E_CUDA, \
     WD_E_NCCL, WD_E_OOM, WD_E_INTERNAL = range(10)
 RULES = {"coupling_cur": 0, "coupling_paper": 1, "verbatim": 2, "full": 3}
+SMOOTHERS = {"fused": 0, "phased": 1}
 ERRNAMES = {1: "WD_E_INVAL", 2: "WD_E_MESH", 3: "WD_E_NOCONV", 4: "WD_E_DIVERGED",
             5: "WD_E_NONFINITE", 6: "WD_E_CUDA", 7: "WD_E_NCCL", 8: "WD_E_OOM",
             9: "WD_E_INTERNAL"}
@@ -38,7 +39,7 @@ class wd_options(C.Structure):
                 ("coarsen_rule", C.c_int), ("use_graph", C.c_int),
                 ("gather_below_nodes", C.c_longlong), ("rank", C.c_int), ("nranks", C.c_int),
                 ("nccl_comm", C.c_void_p), ("j_begin", C.c_int), ("j_end", C.c_int),
-                ("profile", C.c_int)]
+                ("profile", C.c_int), ("smoother", C.c_int)]
 
 
 class wd_report(C.Structure):
@@ -103,7 +104,7 @@ ABI_SYMBOLS = ["wd_default_options", "wd_assemble", "wd_rhs", "wd_vcycle", "wd_s
                "wd_gather_level"]
 
 BENCH_KERNELS = {"gs_sweep": 0, "apply": 1, "restrict": 2, "prolong": 3, "vcycle": 4,
-                 "residual_norm": 5, "galerkin": 6, "assemble": 7}
+                 "residual_norm": 5, "galerkin": 6, "assemble": 7, "gs_sweep_phased": 8}
 
 
 class WDError(RuntimeError):
@@ -140,6 +141,8 @@ def default_options(**kw) -> wd_options:
     for k, v in kw.items():
         if k == "coarsen_rule" and isinstance(v, str):
             v = RULES[v]
+        if k == "smoother" and isinstance(v, str):
+            v = SMOOTHERS[v]
         setattr(o, k, v)
     return o
 

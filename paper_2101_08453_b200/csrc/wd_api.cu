@@ -103,7 +103,8 @@ struct Level {
     double* lam = nullptr;
     double* f = nullptr;
     double* r = nullptr;
-    double* raw[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* lam2 = nullptr;   // second iterate buffer of the fused smoother (ping-pong)
+    double* raw[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     // transition to level + 1
     int hflag = 0;
     int nkept = 0;
@@ -410,12 +411,14 @@ void coarse_range(const std::vector<int>& pos, int a, int b, int& c0, int& c1) {
 
 int alloc_level(wd_ctx* ctx, Level& lv) {
     const size_t nt = (size_t)lv.L.NT;
-    double** arr[4] = {&lv.coef, &lv.lam, &lv.f, &lv.r};
-    const size_t len[4] = {14 * nt, nt, nt, nt};
-    for (int t = 0; t < 4; t++) {
+    double** arr[5] = {&lv.coef, &lv.lam, &lv.f, &lv.r, &lv.lam2};
+    const size_t len[5] = {14 * nt, nt, nt, nt, nt};
+    for (int t = 0; t < 5; t++) {
         RC(dalloc(ctx, (void**)&lv.raw[t], sizeof(double) * len[t]));
         *arr[t] = lv.raw[t];
     }
+    // D entries of the ping-pong buffer stay 0 (the fused sweep writes free nodes only)
+    CK(cudaMemset(lv.lam2, 0, sizeof(double) * nt));
     if (make_coef_maps(lv.L, lv.coef, lv.tmA, lv.tmB) || make_vec_map(lv.L, lv.lam, lv.tmX, true) ||
         make_vec_map(lv.L, lv.f, lv.tmF, false))
         return fail(WD_E_CUDA, "cuTensorMapEncodeTiled failed for level dims (%d,%d,%d)", lv.L.n1,
@@ -555,6 +558,7 @@ int sum_ranks(wd_ctx* ctx, const double* in, double* out, cudaStream_t st) {
 
 // ------------------------------------------------------------------ V-cycle
 int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st);
+int smooth_end(wd_ctx* ctx, int l, cudaStream_t st);
 
 int coarse_solve(wd_ctx* ctx, cudaStream_t st) {
     const int l = ctx->nlev - 1;
@@ -566,23 +570,55 @@ int coarse_solve(wd_ctx* ctx, cudaStream_t st) {
     } else {   // reading C8: GS sweeps from 0 (with halo exchanges on a slab level)
         for (Part& P : ctx->parts) CK(cudaMemsetAsync(P.lev[l].lam, 0, sizeof(double) * P.lev[l].L.NT, st));
         for (int s = 0; s < ctx->opt.coarse_iters; s++) RC(smooth(ctx, l, false, 0, st));
+        RC(smooth_end(ctx, l, st));
     }
     CKL();
     return WD_OK;
 }
 
-// one smoothing sweep on level l: 4 colour phases; on slabs the boundary rows
-// are exchanged after phase 1 (even rows final) and phase 3 (odd rows final)
+// does level l use the fused one-pass sweep (k_gs_fused.cu)?  Slab levels use
+// the four phase launches with their halo exchanges.
+bool fused_level(const wd_ctx* ctx, int l) {
+    return ctx->opt.smoother == WD_SMOOTH_FUSED && !ctx->parts[0].lev[l].dist;
+}
+
+// one smoothing sweep on level l.
+//  * fused: lam -> lam2 in one launch, then the two buffers swap roles (the
+//    caller restores the canonical buffer with smooth_end);
+//  * phased: 4 colour phases in place; on slabs the boundary rows are
+//    exchanged after phase 1 (even rows final) and phase 3 (odd rows final)
 int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st) {
     if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns], st, cudaEventRecordExternal));
-    for (int c = 0; c < 4; c++) {
+    if (fused_level(ctx, l)) {
         for (Part& P : ctx->parts) {
             Level& F = P.lev[l];
-            launch_gs_phase(F.L, F.coef, F.lam, F.f, c, st);
+            launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st);
+            std::swap(F.lam, F.lam2);
         }
-        if (c == 1 || c == 3) RC(exchange(ctx, l, ARR_LAM, 1, st));
+    } else {
+        for (int c = 0; c < 4; c++) {
+            for (Part& P : ctx->parts) {
+                Level& F = P.lev[l];
+                launch_gs_phase(F.L, F.coef, F.lam, F.f, c, st);
+            }
+            if (c == 1 || c == 3) RC(exchange(ctx, l, ARR_LAM, 1, st));
+        }
     }
     if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns + 1], st, cudaEventRecordExternal));
+    return WD_OK;
+}
+
+// after a group of sweeps: the iterate back in the canonical buffer raw[1]
+// (the TMA maps and every other kernel refer to it)
+int smooth_end(wd_ctx* ctx, int l, cudaStream_t st) {
+    for (Part& P : ctx->parts) {
+        Level& F = P.lev[l];
+        if (F.lam != F.raw[1]) {
+            CK(cudaMemcpyAsync(F.raw[1], F.lam, sizeof(double) * F.L.NT, cudaMemcpyDeviceToDevice, st));
+            F.lam2 = F.lam;
+            F.lam = F.raw[1];
+        }
+    }
     return WD_OK;
 }
 
@@ -591,6 +627,7 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st) {
     const bool prof = ctx->opt.profile && l == 0 && ctx->parts.size() == 1;
     int ns = 0;
     for (int s = 0; s < ctx->opt.pre_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
+    RC(smooth_end(ctx, l, st));
     for (Part& P : ctx->parts) apply_level(P.lev[l], true, nullptr, st);
     RC(exchange(ctx, l, ARR_R, 1, st));
     for (Part& P : ctx->parts) {
@@ -609,6 +646,7 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st) {
     }
     RC(exchange(ctx, l, ARR_LAM, 1, st));
     for (int s = 0; s < ctx->opt.post_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
+    RC(smooth_end(ctx, l, st));
     CKL();
     return WD_OK;
 }
@@ -770,6 +808,7 @@ void wd_default_options(wd_options* o) {
     o->gather_below_nodes = 2000000;
     o->rank = 0;
     o->nranks = 1;
+    o->smoother = WD_SMOOTH_FUSED;
 }
 
 const char* wd_last_error(void) { return g_err; }
@@ -1192,7 +1231,8 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
     if (!(a1 > 0 && a2 > 0 && a3 > 0) || !std::isfinite(a1) || !std::isfinite(a2) || !std::isfinite(a3))
         return fail(WD_E_INVAL, "penalty constants must be positive and finite");
     if (opt && (opt->pre_smooth < 0 || opt->post_smooth < 0 || opt->max_cycles < 0 ||
-                opt->coarsen_rule < 0 || opt->coarsen_rule > 3 || opt->coarse_iters < 0))
+                opt->coarsen_rule < 0 || opt->coarsen_rule > 3 || opt->coarse_iters < 0 ||
+                opt->smoother < 0 || opt->smoother > 1))
         return fail(WD_E_INVAL, "invalid options");
     if (opt && opt->coarsest_max_free > 8192)
         return fail(WD_E_INVAL, "coarsest_max_free %d > 8192 (dense inverse)", opt->coarsest_max_free);
@@ -1366,7 +1406,11 @@ int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out)
     CK(cudaEventCreate(&e1));
     auto body = [&]() -> int {
         switch (which) {
-            case 0: launch_gs_sweep(F.L, F.coef, F.lam, F.f, st); break;
+            case 0:   // two sweeps (the V-cycle's pairs: no copy-back), reported per sweep
+                RC(smooth(ctx, level, false, 0, st));
+                RC(smooth(ctx, level, false, 0, st));
+                return smooth_end(ctx, level, st);
+            case 8: launch_gs_sweep(F.L, F.coef, F.lam, F.f, st); break;
             case 1: apply_level(F, true, nullptr, st); break;
             case 2: launch_restrict(F.L, target(P.lev[level + 1]), F.M, F.r, P.lev[level + 1].f, st); break;
             case 3: launch_prolong(F.L, P.lev[level + 1].L, F.M, P.lev[level + 1].lam, F.lam, st); break;
@@ -1390,7 +1434,7 @@ int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out)
     CK(cudaEventSynchronize(e1));
     float ms;
     CK(cudaEventElapsedTime(&ms, e0, e1));
-    *ms_out = ms / reps;
+    *ms_out = ms / reps / (which == 0 ? 2 : 1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     CKL();
@@ -1466,7 +1510,8 @@ int wd_smooth(wd_ctx* ctx, int level, double* x, const double* f, int sweeps, vo
     RC(stage_in(ctx, sf, f, N, st));
     launch_nat2int(lv.L, whole(lv.L, sx.d), lv.lam, true, st);
     launch_nat2int(lv.L, whole(lv.L, sf.d), lv.f, true, st);
-    for (int s = 0; s < sweeps; s++) launch_gs_sweep(lv.L, lv.coef, lv.lam, lv.f, st);
+    for (int s = 0; s < sweeps; s++) RC(smooth(ctx, level, false, 0, st));
+    RC(smooth_end(ctx, level, st));
     sx.out = true;
     sx.host = x;
     launch_int2nat(lv.L, lv.lam, whole(lv.L, sx.d), st);

@@ -129,6 +129,10 @@ void launch_zero_dirichlet(const LevDev& L, double* v, cudaStream_t st);
 void launch_argmin_bottom(const double* Z, int n, double* pval, long long* pidx, int nblk,
                           cudaStream_t st);
 
+// k_gs_fused.cu: one whole 4-colour sweep per launch, lin -> lout (ping-pong)
+void launch_gs_fused(const LevDev& L, const double* coef, const double* lin, double* lout,
+                     const double* f, cudaStream_t st);
+
 // k_apply_tma.cu: TMA-staged residual / apply
 int make_coef_maps(const LevDev& L, const double* coef, void* mapA, void* mapB);
 int make_vec_map(const LevDev& L, const double* v, void* map, bool halo);

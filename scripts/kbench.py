@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--config", default="paper")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--apply-variants", default="")
+    ap.add_argument("--only", default="", help="comma list of level-0 kernels; skip the rest")
     args = ap.parse_args()
     import paper_2101_08453_b200 as wd
     import synth
@@ -27,11 +28,12 @@ def main():
     p = synth.make(args.config, device=dev)
     ctx = wd.wd_assemble(p.X, p.Y, p.Z, p.a)
     f = wd.wd_rhs(ctx, p.u0)
-    lam, rep = wd.wd_solve(ctx, f, rel_tol=1e-8)
+    if not args.only:
+        lam, rep = wd.wd_solve(ctx, f, rel_tol=1e-8)
     n1, n2, n3 = ctx.level_dims(0)
     free0 = (n1 - 2) * (n2 - 2) * (n3 - 1)
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
-    alg = {"gs_sweep": 264 * free0, "apply": 136 * free0, "residual_norm": 128 * free0,
+    alg = {"gs_sweep": 136 * free0, "gs_sweep_phased": 264 * free0, "apply": 136 * free0, "residual_norm": 128 * free0,
            "prolong": 16 * free0, "restrict": 8 * free0 + 8 * free0 // 4}
 
     def report(name, level=0, extra=None):
@@ -44,10 +46,15 @@ def main():
             d.update(extra)
         print(json.dumps(d), flush=True)
 
-    for name in ["gs_sweep", "apply", "residual_norm", "restrict", "prolong", "vcycle"]:
+    if args.only:
+        for name in args.only.split(","):
+            report(name)
+        return
+    for name in ["gs_sweep", "gs_sweep_phased", "apply", "residual_norm", "restrict", "prolong", "vcycle"]:
         report(name)
     for l in range(1, ctx.num_levels() - 1):
         report("gs_sweep", l)
+        report("gs_sweep_phased", l)
     report("assemble")
     for l in range(ctx.num_levels() - 1):
         report("galerkin", l)

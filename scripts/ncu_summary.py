@@ -29,7 +29,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__inst_executed.sum", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
         "launch__shared_mem_per_block_dynamic", "launch__shared_mem_per_block_static"]
 
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6,
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "ns": 1e-6, "us": 1e-3, "ms": 1.0,
          "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
 
 
@@ -94,7 +94,7 @@ def full(path, out, traffic_key=None):
     if traffic_key and first is not None:
         p = os.path.join(ROOT, "profiles", "ncu_gs_traffic.json")
         d = json.load(open(p)) if os.path.exists(p) else {}
-        d[traffic_key] = first
+        d[traffic_key] = first   # key "<kernel>:<config>" (bench.py reads it)
         json.dump(d, open(p, "w"), indent=1)
 
 

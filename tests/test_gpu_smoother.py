@@ -1,0 +1,100 @@
+"""The fused one-pass sweep (k_gs_fused.cu) against the four colour-phase
+launches (k_mg.cu) and the oracle.
+
+The two GPU schedules perform the same floating-point operations in the same
+order for every node (P:174-176 smoother, colour order of reading C7), so the
+iterates must agree BIT FOR BIT on every level, for any number of sweeps and
+any tile raggedness; the oracle agreement (<= 1e-11 relative max per sweep) is
+in test_gpu_parity.py, which runs the default (fused) smoother.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from brute import free_mask
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module")
+def wd():
+    import paper_2101_08453_b200 as m
+    return m
+
+
+GRIDS = {
+    "tiny": lambda: synth.tiny(),
+    "small": lambda: synth.small(),
+    # ragged in i and j against the 64 x 8 tile, odd and even node counts
+    "ragged_a": lambda: synth.hill(nx=150, ny=77, nz=9, dx=40.0, height=200.0, sigma=600.0,
+                                   dz0=8.0, r=1.2, a=(1, 1, 10)),
+    "ragged_b": lambda: synth.hill(nx=65, ny=9, nz=3, dx=30.0, height=80.0, sigma=200.0,
+                                   dz0=5.0, r=1.1, a=(1, 2, 3)),
+    "thin": lambda: synth.hill(nx=3, ny=40, nz=15, dx=30.0, height=50.0, sigma=100.0,
+                               dz0=5.0, r=1.15, a=(1, 1, 1)),
+}
+
+
+def _pair(wd, p, **kw):
+    g = p.to(DEV)
+    out = []
+    for sm in ("fused", "phased"):
+        opt = wd.default_options(coarsest_max_free=60, smoother=sm, **kw)
+        out.append(wd.wd_assemble(g.X, g.Y, g.Z, p.a, opt))
+    return g, out
+
+
+@pytest.mark.parametrize("name", list(GRIDS))
+def test_fused_equals_phased_every_level(wd, name):
+    p = GRIDS[name]()
+    g, (cf, cp) = _pair(wd, p)
+    rng = np.random.default_rng(11)
+    for l in range(cf.num_levels()):
+        n1, n2, n3 = cf.level_dims(l)
+        x = torch.as_tensor(rng.uniform(-1, 1, (n3, n2, n1)), device=DEV)
+        f = torch.as_tensor(rng.uniform(-1, 1, (n3, n2, n1)), device=DEV)
+        for sweeps in (1, 2, 3):
+            a = wd.wd_smooth(cf, l, x.clone(), f, sweeps=sweeps)
+            b = wd.wd_smooth(cp, l, x.clone(), f, sweeps=sweeps)
+            torch.cuda.synchronize()
+            assert torch.equal(a, b), (name, l, sweeps, (a - b).abs().max().item())
+    cf.close()
+    cp.close()
+
+
+@pytest.mark.parametrize("name", ["small", "ragged_a"])
+def test_fused_solve_history_identical(wd, name):
+    p = GRIDS[name]()
+    g, (cf, cp) = _pair(wd, p)
+    f = wd.wd_rhs(cf, g.u0)
+    la, ra = wd.wd_solve(cf, f, rel_tol=1e-10)
+    lb, rb = wd.wd_solve(cp, f, rel_tol=1e-10)
+    torch.cuda.synchronize()
+    assert ra["cycles"] == rb["cycles"]
+    assert ra["hist"] == rb["hist"]
+    assert torch.equal(la, lb)
+    cf.close()
+    cp.close()
+
+
+def test_fused_sweep_matches_oracle_small(wd):
+    """One fused sweep on the fine level of Small against the oracle's GS
+    sweep (<= 1e-11 relative max; the orders differ only by FMA contraction)."""
+    p = synth.small()
+    X, Y, Z, u0 = p.numpy()
+    g = p.to(DEV)
+    ctx = wd.wd_assemble(g.X, g.Y, g.Z, p.a, wd.default_options(smoother="fused"))
+    mg = oracle.MG(X, Y, Z, p.a)
+    rng = np.random.default_rng(5)
+    s = mg.shape(0)
+    x = rng.uniform(-1, 1, s) * free_mask(s)
+    f = rng.uniform(-1, 1, s) * free_mask(s)
+    got = wd.wd_smooth(ctx, 0, torch.as_tensor(x, device=DEV), torch.as_tensor(f, device=DEV),
+                       sweeps=2).cpu().numpy()
+    ref = mg.gs(0, mg.gs(0, x, f), f)
+    assert np.abs(got - ref).max() / np.abs(ref).max() <= 1e-11
+    ctx.close()
