@@ -24,6 +24,11 @@
 //     z needs the NEW values of colours c' < c at planes z-1..z+1 (updated at
 //     steps <= s-1) and the OLD values of colours c' > c at z-1..z+1 (updated
 //     at steps >= s+1), so one barrier per step orders everything;
+//   * persistent CTAs (one per SM) walk their tiles back to back and the
+//     k-pipeline runs on across them: with virtual plane g = k n3 + z (k-th
+//     tile of the CTA), colour c handles g = s - 2c at step s, so the next
+//     tile's first planes are updated while the previous tile's last colours
+//     finish (no per-tile fill/drain or prologue);
 //   * lambda of the tile (+ halo) lives in a 16-plane shared-memory ring,
 //     filled with cp.async five planes ahead; the old iterate is read from one
 //     buffer and the new one written to another (ping-pong), so halo reads
@@ -37,7 +42,10 @@
 //     read ~34 GB).
 #include "wd_internal.cuh"
 
+#include <algorithm>
+
 namespace wd {
+
 
 namespace {
 
@@ -67,78 +75,91 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// issue the copies of plane p (old iterate) of the tile's lambda region
-// (columns I0-3..I0+TI+3, rows J0-1..J0+TJ+1) into its ring slot
-__device__ __forceinline__ void load_plane(const LevDev& L, const double* __restrict__ lin,
-                                           double* ring, int I0, int J0, int p) {
-    double* dst = ring + (p & (RING - 1)) * PL;
-    for (int t = threadIdx.x; t < PL; t += THREADS) {
-        const int lj = t / RW, r = t - lj * RW;
-        const int half = r >= SW, pos = r - half * SW;
-        const int li = 2 * pos + half;
-        const int i = I0 - 4 + li, j = J0 - 1 + lj;
-        if (li >= 1 && i >= 0 && i < L.n1 && j >= 0 && j < L.n2)
-            cp_async8(dst + t, lin + loff(L, i, j, p));
-    }
-}
-
 __global__ void __launch_bounds__(THREADS, 1)
 gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict__ lin,
-                double* __restrict__ lout, const double* __restrict__ f, int jt0) {
+                     double* __restrict__ lout, const double* __restrict__ f, int jt0, int ntx,
+                     int ntiles) {
     extern __shared__ double ring[];
-    const int I0 = blockIdx.x * TI;
-    const int J0 = jt0 + blockIdx.y * TJ;   // local row of an even global row
-    // zero the ring (columns/rows outside the grid stay 0 = never-used values)
     for (int t = threadIdx.x; t < PL * RING; t += THREADS) ring[t] = 0.0;
-    __syncthreads();
 
-    // this thread's colour c and column (i, j)
+    // this thread's colour c and the in-tile offsets (di, dj) of its column:
+    // one warp per (colour, row) over the 32 aligned positions, the last warp
+    // takes the 29 halo columns (colour 0: -2, TI, TI+2; 1: -1, TI+1; 2: TI)
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int c, i, j;
+    int c, di, dj;
     bool inreg = true;
-    if (w < W0) { c = 0; j = J0 + 2 * w; i = I0 + 2 * lane; }
-    else if (w < W1) { c = 1; j = J0 + 2 * (w - W0); i = I0 + 1 + 2 * lane; }
-    else if (w < W2) { c = 2; j = J0 + 1 + 2 * (w - W1); i = I0 + 2 * lane; }
-    else if (w < W3) { c = 3; j = J0 + 1 + 2 * (w - W2); i = I0 + 1 + 2 * lane; }
-    else if (lane < 3 * B0) {           // colour 0 halo: I0-2, I0+TI, I0+TI+2
-        c = 0; j = J0 + 2 * (lane / 3);
+    if (w < W0) { c = 0; dj = 2 * w; di = 2 * lane; }
+    else if (w < W1) { c = 1; dj = 2 * (w - W0); di = 1 + 2 * lane; }
+    else if (w < W2) { c = 2; dj = 1 + 2 * (w - W1); di = 2 * lane; }
+    else if (w < W3) { c = 3; dj = 1 + 2 * (w - W2); di = 1 + 2 * lane; }
+    else if (lane < 3 * B0) {
+        c = 0; dj = 2 * (lane / 3);
         const int e = lane % 3;
-        i = e == 0 ? I0 - 2 : I0 + TI + 2 * e - 2;
-    } else if (lane < 3 * B0 + 2 * B1) {   // colour 1 halo: I0-1, I0+TI+1
+        di = e == 0 ? -2 : TI + 2 * e - 2;
+    } else if (lane < 3 * B0 + 2 * B1) {
         const int q = lane - 3 * B0;
-        c = 1; j = J0 + 2 * (q / 2);
-        i = (q % 2) == 0 ? I0 - 1 : I0 + TI + 1;
-    } else if (lane < NHALO) {          // colour 2 halo: I0+TI
+        c = 1; dj = 2 * (q / 2); di = (q % 2) == 0 ? -1 : TI + 1;
+    } else if (lane < NHALO) {
         const int q = lane - 3 * B0 - 2 * B1;
-        c = 2; j = J0 + 1 + 2 * q; i = I0 + TI;
-    } else { c = 0; j = J0; i = -10; inreg = false; }
+        c = 2; dj = 1 + 2 * q; di = TI;
+    } else { c = 0; dj = 0; di = -10; inreg = false; }
     const int ci = c & 1;
-    const bool active = inreg && i >= 1 && i <= L.n1 - 2 && j >= 0 && j < L.n2 && row_free(L, j);
-    const bool writes = active && i >= I0 && i < I0 + TI && j >= J0 && j < J0 + TJ;
-    const int li = i - I0 + 4, lj = j - J0 + 1;
+    const int li = di + 4, lj = dj + 1;
     const int so = lj * RW + (li & 1) * SW + (li >> 1);
-    // offsets of the neighbour column (dx,dy), dx,dy in -1..1, in the ring
-    // (smem) and in the i-split layout (global): the column i-1 / i+1 lives
-    // in the other parity half
     const int sxm = ci ? -SW : SW - 1, sxp = ci ? 1 - SW : SW;
     const int gxm = ci ? -L.H : L.H - 1, gxp = ci ? 1 - L.H : L.H;
     const int gsj = (int)L.sj;
     auto sc = [&](int dx, int dy) { return dy * RW + (dx < 0 ? sxm : dx > 0 ? sxp : 0); };
     auto co = [&](int dx, int dy) { return dy * gsj + (dx < 0 ? gxm : dx > 0 ? gxp : 0); };
-    const i64 own = active ? loff(L, i, j, 0) : 0;
     const i64 NT = L.NT;
-    const int nz = L.n3 - 1;   // free planes 0..nz-1 (top plane n3-1 is Dirichlet)
+    const int n3 = L.n3, nz = L.n3 - 1;
+    const int ntk = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int G = ntk * n3;
 
-    // lambda planes stream in LA planes ahead, one cp.async group per plane
+    // tile k of this CTA -> origin (I0, J0)
+    auto origin = [&](int k, int& I0, int& J0) {
+        const int tau = (int)blockIdx.x + k * (int)gridDim.x;
+        const int ty = tau / ntx;
+        I0 = (tau - ty * ntx) * TI;
+        J0 = jt0 + ty * TJ;
+    };
+    // this thread's column in tile k: active / writes / offset of plane 0
+    bool act = false, wrt = false;
+    i64 own = 0;
+    auto set_tile = [&](int k) {
+        int I0, J0;
+        origin(k, I0, J0);
+        const int i = I0 + di, j = J0 + dj;
+        act = inreg && i >= 1 && i <= L.n1 - 2 && j >= 0 && j < L.n2 && row_free(L, j);
+        wrt = act && di >= 0 && di < TI && dj < TJ;
+        own = act ? loff(L, i, j, 0) : 0;
+    };
+    // lambda load stream: virtual plane gl = (kl, zl) of tile origin (lI0, lJ0)
+    int kl = 0, zl = 0, lI0 = 0, lJ0 = 0;
+    if (G > 0) origin(0, lI0, lJ0);
+    auto load_next = [&]() {
+        double* dst = ring + ((kl * n3 + zl) & (RING - 1)) * PL;
+        for (int t = threadIdx.x; t < PL; t += THREADS) {
+            const int rj = t / RW, r = t - rj * RW;
+            const int half = r >= SW, pos = r - half * SW;
+            const int ri = 2 * pos + half;
+            const int i = lI0 - 4 + ri, j = lJ0 - 1 + rj;
+            if (ri >= 1 && i >= 0 && i < L.n1 && j >= 0 && j < L.n2) cp_async8(dst + t, lin + loff(L, i, j, zl));
+            else dst[t] = 0.0;
+        }
+        if (++zl == n3) {
+            zl = 0;
+            if (++kl < ntk) origin(kl, lI0, lJ0);
+        }
+    };
+    __syncthreads();   // ring zeroed before the first copies land
     for (int p = 0; p < LA; p++) {
-        if (p <= L.n3 - 1) load_plane(L, lin, ring, I0, J0, p);
+        if (p < G) load_next();
         cp_async_commit();
     }
-    cp_async_wait<LA - 2>();   // planes 0, 1
+    cp_async_wait<LA - 2>();
     __syncthreads();
 
-    // couplings (forward kf stored here, backward kb stored at the neighbours),
-    // f and the diagonal of the node this thread updates next
     double kf[13], kb[13], fv = 0.0, kd = 1.0;
     auto load_k = [&](int z) {
         const i64 base = own + (i64)z * L.sk;
@@ -153,41 +174,50 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
         fv = __ldg(f + base);
         kd = __ldg(K + base);
     };
-    if (active && c == 0) load_k(0);
+    // the thread's next node: plane zn of its kn-th tile (virtual plane s - 2c)
+    int kn = 0, zn = 0;
+    if (G > 0) set_tile(0);
+    if (c == 0 && act && G > 0) load_k(0);
 
-    const int nsteps = nz + LAG * 3;
+    const int nsteps = G + LAG * 3;
     for (int s = 0; s < nsteps; s++) {
-        if (s + LA <= L.n3 - 1) load_plane(L, lin, ring, I0, J0, s + LA);
+        if (s + LA < G) load_next();
         cp_async_commit();
-        const int z = s - LAG * c;
-        if (active && z >= 0 && z < nz) {
-            const double* r1 = ring + ((z + 1) & (RING - 1)) * PL + so;
-            const double* r0 = ring + (z & (RING - 1)) * PL + so;
-            const double* rm = ring + ((z - 1) & (RING - 1)) * PL + so;
-            double acc = 0.0;
-            // forward couplings K(p, p + d_s) stored at p  (same order as gs_phase_kernel)
+        const int g = s - LAG * c;
+        if (g >= 0 && g < G) {
+            const int z = zn;
+            if (z < nz && act) {
+                const double* r1 = ring + ((g + 1) & (RING - 1)) * PL + so;
+                const double* r0 = ring + (g & (RING - 1)) * PL + so;
+                const double* rm = ring + ((g - 1) & (RING - 1)) * PL + so;
+                double acc = 0.0;
 #pragma unroll
-            for (int sl = 1; sl < 14; sl++) {
-                const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
-                acc = fma(kf[sl - 1], (dz ? r1 : r0)[sc(dx, dy)], acc);
-            }
-            // backward couplings K(p, p - d_s) stored at p - d_s
-#pragma unroll
-            for (int sl = 1; sl < 14; sl++) {
-                const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
-                if (dz) {
-                    if (z > 0) acc = fma(kb[sl - 1], rm[sc(-dx, -dy)], acc);
-                } else {
-                    acc = fma(kb[sl - 1], r0[sc(-dx, -dy)], acc);
+                for (int sl = 1; sl < 14; sl++) {
+                    const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+                    acc = fma(kf[sl - 1], (dz ? r1 : r0)[sc(dx, dy)], acc);
                 }
+#pragma unroll
+                for (int sl = 1; sl < 14; sl++) {
+                    const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+                    if (dz) {
+                        if (z > 0) acc = fma(kb[sl - 1], rm[sc(-dx, -dy)], acc);
+                    } else {
+                        acc = fma(kb[sl - 1], r0[sc(-dx, -dy)], acc);
+                    }
+                }
+                const double v = (fv - acc) / kd;
+                ring[(g & (RING - 1)) * PL + so] = v;
+                if (wrt) lout[own + (i64)z * L.sk] = v;
             }
-            const double v = (fv - acc) / kd;
-            ring[(z & (RING - 1)) * PL + so] = v;
-            if (writes) lout[own + (i64)z * L.sk] = v;
+            if (++zn == n3) {
+                zn = 0;
+                if (++kn < ntk) set_tile(kn);
+            }
+            if (g + 1 < G && zn < nz && act) load_k(zn);
+        } else if (g == -1 && act && G > 0) {
+            load_k(0);   // colours c > 0: first node, one step ahead
         }
-        // next plane's couplings, issued before the barrier that precedes their use
-        if (active && z + 1 >= 0 && z + 1 < nz) load_k(z + 1);
-        cp_async_wait<LA - 2>();   // planes <= s + 2 (needed by step s + 1)
+        cp_async_wait<LA - 2>();
         __syncthreads();
     }
     cp_async_wait<0>();
@@ -199,16 +229,20 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
 // free nodes; D entries of lout must already be 0)
 void launch_gs_fused(const LevDev& L, const double* coef, const double* lin, double* lout,
                      const double* f, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static int nsm = 0;
+    if (!nsm) {
         cudaFuncSetAttribute(gs_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        attr = true;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (nsm <= 0) nsm = 148;
     }
     // tiles of TJ rows from the even global row at or below the first owned row
     const int jt0 = L.own0 - ((L.own0 + L.jg0) & 1);
-    dim3 grid((L.n1 + TI - 1) / TI, (L.own1 - jt0 + TJ - 1) / TJ);
+    const int ntx = (L.n1 + TI - 1) / TI, nty = (L.own1 - jt0 + TJ - 1) / TJ;
     g_launches += 1;
-    gs_fused_kernel<<<grid, THREADS, SMEM, st>>>(L, coef, lin, lout, f, jt0);
+    const int grid = std::min(ntx * nty, nsm);   // persistent: one CTA per SM
+    gs_fused_kernel<<<grid, THREADS, SMEM, st>>>(L, coef, lin, lout, f, jt0, ntx, ntx * nty);
 }
 
 }  // namespace wd
