@@ -300,12 +300,82 @@ __device__ __forceinline__ double kget(const LevDev& L, const double* __restrict
     return ldg(K + (-s) * L.NT + loff(L, i + dx, j + dy, k + dz));
 }
 
+// 1-D pair lists of the Galerkin product for a regular coarse index (coarse
+// neighbours at fine distance 2 on both sides, so the support of I is the
+// fine offsets -1, 0, 1 with weights 1/2, 1, 1/2 around pos(I)): for coarse
+// offset D the pairs (u, v) = (offset of a node of supp(I), offset of a node
+// of supp(I+D)), both relative to pos(I), with |v - u| <= 1, and the product
+// of their weights, in the order support1d/galerkin_kernel enumerate them
+// (u major, both ascending).
+struct Pair1 { int u, v; double w; };
+
+template <int D>
+__device__ __forceinline__ constexpr int npairs() { return D == 0 ? 7 : 3; }
+template <int D>
+__device__ __forceinline__ Pair1 pair(int n) {
+    // compile-time tables (the loops below are fully unrolled)
+    constexpr Pair1 P0[7] = {{-1, -1, 0.25}, {-1, 0, 0.5}, {0, -1, 0.5}, {0, 0, 1.0},
+                             {0, 1, 0.5}, {1, 0, 0.5}, {1, 1, 0.25}};
+    constexpr Pair1 PP[3] = {{0, 1, 0.5}, {1, 1, 0.25}, {1, 2, 0.5}};
+    constexpr Pair1 PM[3] = {{-1, -2, 0.5}, {-1, -1, 0.25}, {0, -1, 0.5}};
+    return D == 0 ? P0[n] : D > 0 ? PP[n] : PM[n];
+}
+
+// K_c(I, I + (DX, DY, DZ)) for a coarse node whose x and y supports are
+// regular and whose z map is the identity: the same products and sums in the
+// same order as the generic loop of galerkin_kernel (bitwise equal), with
+// every index a compile-time offset.
+template <int DX, int DY, int DZ>
+__device__ __forceinline__ double galerkin_regular(const LevDev& F, const double* __restrict__ K,
+                                                   int fi, int fj, int k) {
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < npairs<DY>(); b++) {
+        const Pair1 py = pair<DY>(b);
+        double sr = 0.0;
+#pragma unroll
+        for (int a = 0; a < npairs<DX>(); a++) {
+            const Pair1 px = pair<DX>(a);
+            sr = fma(px.w, kget(F, K, fi + px.u, fj + py.u, k, px.v - px.u, py.v - py.u, DZ), sr);
+        }
+        s = fma(1.0 * py.w, sr, s);
+    }
+    return s;
+}
+
+// is coarse index c regular along a direction (kept fine indices of c-1..c+2 at spacing 2)?
+__device__ __forceinline__ bool regular1d(const int* __restrict__ pos, int nc, int c) {
+    if (c < 1 || c + 2 > nc - 1) return false;
+    const int p = pos[c];
+    return pos[c - 1] == p - 2 && pos[c + 1] == p + 2 && pos[c + 2] == p + 4;
+}
+
 __global__ void __launch_bounds__(128)
 galerkin_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ KF,
-                double* __restrict__ KC) {
+                double* __restrict__ KC, int zident) {
     const int I = blockIdx.x * 128 + threadIdx.x;
     const int J = blockIdx.y, Kc = blockIdx.z;
     if (I < 1 || I > C.n1 - 2 || !row_free(C, J) || Kc > C.n3 - 2) return;
+    if (zident && regular1d(M.pos[0], C.n1, I) && regular1d(M.pos[1], C.n2, J)) {
+        const int fi = M.pos[0][I], fj = M.pos[1][J];
+        const i64 out = loff(C, I, J, Kc);
+        double* o = KC + out;
+        o[0 * C.NT] = galerkin_regular<0, 0, 0>(F, KF, fi, fj, Kc);
+        o[1 * C.NT] = galerkin_regular<1, 0, 0>(F, KF, fi, fj, Kc);
+        o[2 * C.NT] = galerkin_regular<-1, 1, 0>(F, KF, fi, fj, Kc);
+        o[3 * C.NT] = galerkin_regular<0, 1, 0>(F, KF, fi, fj, Kc);
+        o[4 * C.NT] = galerkin_regular<1, 1, 0>(F, KF, fi, fj, Kc);
+        o[5 * C.NT] = galerkin_regular<-1, -1, 1>(F, KF, fi, fj, Kc);
+        o[6 * C.NT] = galerkin_regular<0, -1, 1>(F, KF, fi, fj, Kc);
+        o[7 * C.NT] = galerkin_regular<1, -1, 1>(F, KF, fi, fj, Kc);
+        o[8 * C.NT] = galerkin_regular<-1, 0, 1>(F, KF, fi, fj, Kc);
+        o[9 * C.NT] = galerkin_regular<0, 0, 1>(F, KF, fi, fj, Kc);
+        o[10 * C.NT] = galerkin_regular<1, 0, 1>(F, KF, fi, fj, Kc);
+        o[11 * C.NT] = galerkin_regular<-1, 1, 1>(F, KF, fi, fj, Kc);
+        o[12 * C.NT] = galerkin_regular<0, 1, 1>(F, KF, fi, fj, Kc);
+        o[13 * C.NT] = galerkin_regular<1, 1, 1>(F, KF, fi, fj, Kc);
+        return;
+    }
     int pt[3][3];
     double pw[3][3];
     int pm[3];
@@ -489,10 +559,10 @@ void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const do
 }
 
 void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* coefF,
-                     double* coefC, unsigned int*, cudaStream_t st) {
+                     double* coefC, int zident, cudaStream_t st) {
     dim3 grid((Cl.n1 + 127) / 128, Cl.n2, Cl.n3);
     g_launches += 1;
-    galerkin_kernel<<<grid, 128, 0, st>>>(F, Cl, M, coefF, coefC);
+    galerkin_kernel<<<grid, 128, 0, st>>>(F, Cl, M, coefF, coefC, zident && !g_galerkin_generic);
 }
 
 void launch_export27(const LevDev& L, const double* coef, double* K27, cudaStream_t st) {

@@ -215,6 +215,7 @@ struct wd_ctx {
 namespace wd {
 std::atomic<long long> g_launches{0};
 int g_apply_variant = 1;
+int g_galerkin_generic = 0;
 }
 
 namespace {
@@ -1184,7 +1185,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
                 F.M.co[d] = F.dmap + offs[d][1];
                 F.M.pos[d] = F.dmap + offs[d][2];
             }
-            launch_galerkin(F.L, target(C), F.M, F.coef, C.coef, nullptr, st);
+            launch_galerkin(F.L, target(C), F.M, F.coef, C.coef, nk == fn3, st);
             CKL();
         }
         ctx->nlev++;
@@ -1225,6 +1226,7 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
     *out = nullptr;
     if (const char* v = getenv("WD_APPLY_VARIANT")) g_apply_variant = atoi(v);
     if (const char* v = getenv("WD_TMA_DEBUG")) g_tma_debug = atoi(v);
+    g_galerkin_generic = getenv("WD_GALERKIN_GENERIC") ? atoi(getenv("WD_GALERKIN_GENERIC")) : 0;
     if (!X || !Y || !Z) return fail(WD_E_INVAL, "NULL coordinate array");
     if (n1 < 3 || n2 < 3 || n3 < 2) return fail(WD_E_INVAL, "dims (%d,%d,%d): need n1,n2 >= 3, n3 >= 2", n1, n2, n3);
     if (n3 - 1 >= MAXNZ) return fail(WD_E_INVAL, "n3 = %d exceeds %d", n3, MAXNZ);
@@ -1416,7 +1418,7 @@ int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out)
             case 3: launch_prolong(F.L, P.lev[level + 1].L, F.M, P.lev[level + 1].lam, F.lam, st); break;
             case 4: return run_vcycle(ctx, st);
             case 5: return residual_sq(ctx, 0, st);
-            case 6: launch_galerkin(F.L, target(P.lev[level + 1]), F.M, F.coef, P.lev[level + 1].coef, nullptr, st); break;
+            case 6: launch_galerkin(F.L, target(P.lev[level + 1]), F.M, F.coef, P.lev[level + 1].coef, F.nkept == F.L.n3, st); break;
             case 7: {
                 unsigned long long* dbad = (unsigned long long*)(ctx->dscal + 8);
                 launch_assemble(P.X, P.Y, P.Z, ctx->n1, ctx->n2, ctx->n3, ctx->c, P.lev[0].L,

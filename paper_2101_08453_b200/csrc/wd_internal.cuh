@@ -25,6 +25,7 @@ extern std::atomic<long long> g_launches;
 // development knob: thread mapping of apply_kernel (env WD_APPLY_VARIANT)
 extern int g_apply_variant;
 extern int g_tma_debug;
+extern int g_galerkin_generic;   // env WD_GALERKIN_GENERIC=1: disable the unrolled path (tests)
 
 typedef long long i64;
 
@@ -122,8 +123,10 @@ void launch_restrict(const LevDev& F, const LevDev& Cl, const MapDev& M, const d
                      double* fc, cudaStream_t st);
 void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* xc,
                     double* x, cudaStream_t st);
+// zident: the z map of this transition is the identity (no layer merged);
+// regular interior columns then take an unrolled path (bitwise equal)
 void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* coefF,
-                     double* coefC, unsigned int* overflow, cudaStream_t st);
+                     double* coefC, int zident, cudaStream_t st);
 void launch_export27(const LevDev& L, const double* coef, double* K27, cudaStream_t st);
 void launch_zero_dirichlet(const LevDev& L, double* v, cudaStream_t st);
 void launch_argmin_bottom(const double* Z, int n, double* pval, long long* pidx, int nblk,
