@@ -229,6 +229,13 @@ __global__ void zero_dirichlet_kernel(LevDev L, double* v) {
     if (i == 0 || i == L.n1 - 1 || row_dirichlet(L, j) || k == L.n3 - 1) v[loff(L, i, j, k)] = 0.0;
 }
 
+// is coarse index c regular along a direction (kept fine indices of c-1..c+2 at spacing 2)?
+__device__ __forceinline__ bool regular1d(const int* __restrict__ pos, int nc, int c) {
+    if (c < 1 || c + 2 > nc - 1) return false;
+    const int p = pos[c];
+    return pos[c - 1] == p - 2 && pos[c + 1] == p + 2 && pos[c + 2] == p + 4;
+}
+
 // 1-D support of coarse index c along one direction: fine indices and weights
 __device__ __forceinline__ int support1d(const int* __restrict__ pos, const int* __restrict__ co,
                                          int n, int c, int (&t)[3], double (&w)[3]) {
@@ -242,10 +249,28 @@ __device__ __forceinline__ int support1d(const int* __restrict__ pos, const int*
 
 __global__ void __launch_bounds__(128)
 restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
-                double* __restrict__ fc) {
+                double* __restrict__ fc, int zident) {
     const int I = blockIdx.x * 128 + threadIdx.x;
     const int J = blockIdx.y;
     if (I < 1 || I > C.n1 - 2 || !row_free(C, J)) return;
+    if (zident && regular1d(M.pos[0], C.n1, I) && regular1d(M.pos[1], C.n2, J)) {
+        // regular supports {-1, 0, 1} x {-1, 0, 1}, weights (1/2, 1, 1/2), identity in z:
+        // the generic loop below with compile-time weights (same order, bitwise equal)
+        const double w[3] = {0.5, 1.0, 0.5};
+        const int fi = M.pos[0][I], fj = M.pos[1][J];
+        for (int Kc = 0; Kc <= C.n3 - 2; Kc++) {
+            double s = 0.0;
+#pragma unroll
+            for (int b = 0; b < 3; b++) {
+                double sr = 0.0;
+#pragma unroll
+                for (int a = 0; a < 3; a++) sr = fma(w[a], ldg(r + loff(F, fi + a - 1, fj + b - 1, Kc)), sr);
+                s = fma(1.0 * w[b], sr, s);
+            }
+            fc[loff(C, I, J, Kc)] = s;
+        }
+        return;
+    }
     int tx[3], ty[3];
     double wx[3], wy[3];
     const int mx = support1d(M.pos[0], M.co[0], F.n1, I, tx, wx);
@@ -268,13 +293,26 @@ restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
 
 __global__ void __launch_bounds__(128)
 prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
-               double* __restrict__ x) {
+               double* __restrict__ x, int zident) {
     const int i = blockIdx.x * 128 + threadIdx.x;
     const int j = blockIdx.y;
     if (i < 1 || i > F.n1 - 2 || !row_free(F, j)) return;
     const int ix = M.lo[0][i], iy = M.lo[1][j];
     const int nx = M.co[0][i] ? 1 : 2, ny = M.co[1][j] ? 1 : 2;
     const double wx = nx == 1 ? 1.0 : 0.5, wy = ny == 1 ? 1.0 : 0.5;
+    if (zident) {
+        // identity in z (no layer merged): the loop below with iz = k, one z term
+        for (int k = 0; k <= F.n3 - 2; k++) {
+            double s = 0.0;
+            for (int b = 0; b < ny; b++) {
+                double sr = 0.0;
+                for (int a = 0; a < nx; a++) sr += ldg(xc + loff(C, ix + a, iy + b, k));
+                s = fma(wy * 1.0, wx * sr, s);
+            }
+            x[loff(F, i, j, k)] += s;
+        }
+        return;
+    }
 #pragma unroll 4
     for (int k = 0; k <= F.n3 - 2; k++) {
         const int iz = M.lo[2][k];
@@ -341,13 +379,6 @@ __device__ __forceinline__ double galerkin_regular(const LevDev& F, const double
         s = fma(1.0 * py.w, sr, s);
     }
     return s;
-}
-
-// is coarse index c regular along a direction (kept fine indices of c-1..c+2 at spacing 2)?
-__device__ __forceinline__ bool regular1d(const int* __restrict__ pos, int nc, int c) {
-    if (c < 1 || c + 2 > nc - 1) return false;
-    const int p = pos[c];
-    return pos[c - 1] == p - 2 && pos[c + 1] == p + 2 && pos[c + 2] == p + 4;
 }
 
 __global__ void __launch_bounds__(128)
@@ -545,17 +576,17 @@ void launch_norm2_partial(const LevDev& L, const double* v, double* partial, int
 }
 
 void launch_restrict(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* r,
-                     double* fc, cudaStream_t st) {
+                     double* fc, int zident, cudaStream_t st) {
     dim3 grid((Cl.n1 + 127) / 128, Cl.n2);
     g_launches += 1;
-    restrict_kernel<<<grid, 128, 0, st>>>(F, Cl, M, r, fc);
+    restrict_kernel<<<grid, 128, 0, st>>>(F, Cl, M, r, fc, zident);
 }
 
 void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* xc,
-                    double* x, cudaStream_t st) {
+                    double* x, int zident, cudaStream_t st) {
     dim3 grid((F.n1 + 127) / 128, F.n2);
     g_launches += 1;
-    prolong_kernel<<<grid, 128, 0, st>>>(F, Cl, M, xc, x);
+    prolong_kernel<<<grid, 128, 0, st>>>(F, Cl, M, xc, x, zident);
 }
 
 void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* coefF,

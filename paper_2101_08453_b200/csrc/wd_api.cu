@@ -634,7 +634,7 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st) {
     for (Part& P : ctx->parts) {
         Level& F = P.lev[l];
         Level& C = P.lev[l + 1];
-        launch_restrict(F.L, target(C), F.M, F.r, C.f, st);
+        launch_restrict(F.L, target(C), F.M, F.r, C.f, F.nkept == F.L.n3, st);
     }
     if (l + 1 == ctx->gather) RC(gather_rows(ctx, l + 1, ARR_F, st));
     for (Part& P : ctx->parts) CK(cudaMemsetAsync(P.lev[l + 1].lam, 0, sizeof(double) * P.lev[l + 1].L.NT, st));
@@ -643,7 +643,7 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st) {
     for (Part& P : ctx->parts) {
         Level& F = P.lev[l];
         Level& C = P.lev[l + 1];
-        launch_prolong(F.L, C.L, F.M, C.lam, F.lam, st);
+        launch_prolong(F.L, C.L, F.M, C.lam, F.lam, F.nkept == F.L.n3, st);
     }
     RC(exchange(ctx, l, ARR_LAM, 1, st));
     for (int s = 0; s < ctx->opt.post_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
@@ -1414,8 +1414,8 @@ int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out)
                 return smooth_end(ctx, level, st);
             case 8: launch_gs_sweep(F.L, F.coef, F.lam, F.f, st); break;
             case 1: apply_level(F, true, nullptr, st); break;
-            case 2: launch_restrict(F.L, target(P.lev[level + 1]), F.M, F.r, P.lev[level + 1].f, st); break;
-            case 3: launch_prolong(F.L, P.lev[level + 1].L, F.M, P.lev[level + 1].lam, F.lam, st); break;
+            case 2: launch_restrict(F.L, target(P.lev[level + 1]), F.M, F.r, P.lev[level + 1].f, F.nkept == F.L.n3, st); break;
+            case 3: launch_prolong(F.L, P.lev[level + 1].L, F.M, P.lev[level + 1].lam, F.lam, F.nkept == F.L.n3, st); break;
             case 4: return run_vcycle(ctx, st);
             case 5: return residual_sq(ctx, 0, st);
             case 6: launch_galerkin(F.L, target(P.lev[level + 1]), F.M, F.coef, P.lev[level + 1].coef, F.nkept == F.L.n3, st); break;
@@ -1533,7 +1533,7 @@ int wd_restrict(wd_ctx* ctx, int level, const double* r, double* fc, void* strea
     RC(stage_out(ctx, sc, fc, nodes_of(C.L)));
     launch_nat2int(F.L, whole(F.L, sr.d), F.r, true, st);
     CK(cudaMemsetAsync(C.f, 0, sizeof(double) * C.L.NT, st));
-    launch_restrict(F.L, target(C), F.M, F.r, C.f, st);
+    launch_restrict(F.L, target(C), F.M, F.r, C.f, F.nkept == F.L.n3, st);
     launch_int2nat(C.L, C.f, whole(C.L, sc.d), st);
     CKL();
     return stage_finish(st, {&sr, &sc});
@@ -1551,7 +1551,7 @@ int wd_prolong(wd_ctx* ctx, int level, const double* xc, double* x, void* stream
     RC(stage_in(ctx, sx, x, nodes_of(F.L), st));
     launch_nat2int(C.L, whole(C.L, sc.d), C.lam, true, st);
     launch_nat2int(F.L, whole(F.L, sx.d), F.lam, true, st);
-    launch_prolong(F.L, C.L, F.M, C.lam, F.lam, st);
+    launch_prolong(F.L, C.L, F.M, C.lam, F.lam, F.nkept == F.L.n3, st);
     sx.out = true;
     sx.host = x;
     launch_int2nat(F.L, F.lam, whole(F.L, sx.d), st);

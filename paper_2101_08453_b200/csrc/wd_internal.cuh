@@ -119,10 +119,11 @@ struct MapDev {
     const int* co[3];
     const int* pos[3];
 };
+// zident: the z map of the transition is the identity (fast paths, bitwise equal)
 void launch_restrict(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* r,
-                     double* fc, cudaStream_t st);
+                     double* fc, int zident, cudaStream_t st);
 void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* xc,
-                    double* x, cudaStream_t st);
+                    double* x, int zident, cudaStream_t st);
 // zident: the z map of this transition is the identity (no layer merged);
 // regular interior columns then take an unrolled path (bitwise equal)
 void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* coefF,
