@@ -301,15 +301,27 @@ prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
     const int nx = M.co[0][i] ? 1 : 2, ny = M.co[1][j] ? 1 : 2;
     const double wx = nx == 1 ? 1.0 : 0.5, wy = ny == 1 ? 1.0 : 0.5;
     if (zident) {
-        // identity in z (no layer merged): the loop below with iz = k, one z term
+        // identity in z (no layer merged): the loop below with iz = k and one z
+        // term, branch-free in x (even and odd i share a warp; adding -0.0 is
+        // the identity, so the sums are those of the generic loop bit for bit)
+        const double* c0 = xc + loff(C, ix, iy, 0);
+        const double* c1 = xc + loff(C, ix + nx - 1, iy, 0);
+        const double* c2 = xc + loff(C, ix, iy + ny - 1, 0);
+        const double* c3 = xc + loff(C, ix + nx - 1, iy + ny - 1, 0);
+        double* xo = x + loff(F, i, j, 0);
+        const bool two = nx == 2;
+#pragma unroll 4
         for (int k = 0; k <= F.n3 - 2; k++) {
-            double s = 0.0;
-            for (int b = 0; b < ny; b++) {
-                double sr = 0.0;
-                for (int a = 0; a < nx; a++) sr += ldg(xc + loff(C, ix + a, iy + b, k));
-                s = fma(wy * 1.0, wx * sr, s);
+            const i64 kc = (i64)k * C.sk;
+            double sr = 0.0 + ldg(c0 + kc);
+            sr += two ? ldg(c1 + kc) : -0.0;
+            double s = fma(wy * 1.0, wx * sr, 0.0);
+            if (ny == 2) {
+                double sr2 = 0.0 + ldg(c2 + kc);
+                sr2 += two ? ldg(c3 + kc) : -0.0;
+                s = fma(wy * 1.0, wx * sr2, s);
             }
-            x[loff(F, i, j, k)] += s;
+            xo[(i64)k * F.sk] += s;
         }
         return;
     }
