@@ -40,7 +40,7 @@ CONFIG_NAMES = {"tiny": "tiny 16x16x8 (configs[0])", "small": "small 128x128x10 
                 "paper": "paper-scale 3000x3000x15 (configs[3])"}
 # algorithmic HBM bytes per free node of one launch of the level-0 smoother:
 #   fused sweep (1 launch/sweep): 14 stored couplings (112) + f (8) + lambda read + write (16)
-#   colour phase (4 launches/sweep, slab levels): 264 B/node/sweep / 4
+#   colour phase (4 launches/sweep, --smoother phased): 264 B/node/sweep / 4
 GS_BYTES = {"fused": (136, 1, "gs_fused_kernel"), "phased": (66, 4, "gs_phase_kernel")}
 CPU_CROP = 200                            # oracle sample: 200x200x15 elements of the workload
 
@@ -294,15 +294,15 @@ def run_ours(args, ws, rank, local):
     ms_step = ms_total / args.steps
     value = nodes * (cycles / args.steps) / (ms_step * 1e-3)   # one global grid on ws GPUs
 
-    # roofline of the dominant kernel: the level-0 smoother launch (one fused sweep;
-    # one colour phase on slab levels, which always use the phased schedule)
+    # roofline of the dominant kernel: the level-0 smoother launch (one fused sweep,
+    # or one colour phase with --smoother phased)
     peak, peak_src = measured_hbm_peak()
     n1, _, n3 = prob.dims
     if ws > 1:   # this rank's free rows
         free0 = (n1 - 2) * (min(je, n2 - 1) - max(jb, 1)) * (n3 - 1)
     else:
         free0 = (n1 - 2) * (n2 - 2) * (n3 - 1)
-    gs_kind = "fused" if (args.smoother == "fused" and ws == 1) else "phased"
+    gs_kind = args.smoother
     gs_b, gs_per_sweep, gs_name = GS_BYTES[gs_kind]
     launch_ms = gs_ms / max(gs_sweeps, 1) / gs_per_sweep
     bytes_launch = gs_b * free0

@@ -63,10 +63,10 @@ enum { WD_RULE_COUPLING_CUR = 0, WD_RULE_COUPLING_PAPER = 1, WD_RULE_VERBATIM = 
 /* Schedule of the 4-colour smoother.  Both compute the same
  * iterate bit for bit (same operations in the same order per node):
  *  FUSED   one launch per sweep: all four colour phases pipelined over k in
- *          shared-memory tiles (k_gs_fused.cu); used on every level that is
- *          not split into slabs (default)
+ *          shared-memory tiles (k_gs_fused.cu); on slab levels one 2-row halo
+ *          exchange of lambda per sweep (default)
  *  PHASED  four launches per sweep, one per colour (k_mg.cu gs_phase_kernel);
- *          always used on slab levels */
+ *          on slab levels halo rows exchanged after colours 1 and 3 */
 enum { WD_SMOOTH_FUSED = 0, WD_SMOOTH_PHASED = 1 };
 
 typedef struct wd_ctx wd_ctx;

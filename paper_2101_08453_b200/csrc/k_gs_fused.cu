@@ -130,8 +130,14 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
         int I0, J0;
         origin(k, I0, J0);
         const int i = I0 + di, j = J0 + dj;
-        act = inreg && i >= 1 && i <= L.n1 - 2 && j >= 0 && j < L.n2 && row_free(L, j);
-        wrt = act && di >= 0 && di < TI && dj < TJ;
+        // computed: a free node whose rows j-1, j+1 are present in this part
+        // (on a slab the halo rows next to the owned ones are recomputed as
+        // tile halo; their inputs come from the 2-row exchange before the sweep)
+        const int jg = j + L.jg0;
+        act = inreg && i >= 1 && i <= L.n1 - 2 && j >= 1 && j <= L.n2 - 2 && jg >= 1 &&
+              jg <= L.n2g - 2;
+        // written: owned rows of the tile's own region only
+        wrt = act && di >= 0 && di < TI && dj < TJ && j >= L.own0 && j < L.own1;
         own = act ? loff(L, i, j, 0) : 0;
     };
     // lambda load stream: virtual plane gl = (kl, zl) of tile origin (lI0, lJ0)

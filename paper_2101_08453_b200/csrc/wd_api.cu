@@ -577,20 +577,20 @@ int coarse_solve(wd_ctx* ctx, cudaStream_t st) {
     return WD_OK;
 }
 
-// does level l use the fused one-pass sweep (k_gs_fused.cu)?  Slab levels use
-// the four phase launches with their halo exchanges.
-bool fused_level(const wd_ctx* ctx, int l) {
-    return ctx->opt.smoother == WD_SMOOTH_FUSED && !ctx->parts[0].lev[l].dist;
-}
+// does level l use the fused one-pass sweep (k_gs_fused.cu)?
+bool fused_level(const wd_ctx* ctx, int l) { return ctx->opt.smoother == WD_SMOOTH_FUSED; }
 
 // one smoothing sweep on level l.
 //  * fused: lam -> lam2 in one launch, then the two buffers swap roles (the
-//    caller restores the canonical buffer with smooth_end);
+//    caller restores the canonical buffer with smooth_end); on slabs the two
+//    halo rows of the input iterate are exchanged first (the sweep recomputes
+//    the nearest halo row as tile halo and writes owned rows only);
 //  * phased: 4 colour phases in place; on slabs the boundary rows are
 //    exchanged after phase 1 (even rows final) and phase 3 (odd rows final)
 int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st) {
     if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns], st, cudaEventRecordExternal));
     if (fused_level(ctx, l)) {
+        RC(exchange(ctx, l, ARR_LAM, 2, st));
         for (Part& P : ctx->parts) {
             Level& F = P.lev[l];
             launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st);
@@ -610,7 +610,8 @@ int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st) {
 }
 
 // after a group of sweeps: the iterate back in the canonical buffer raw[1]
-// (the TMA maps and every other kernel refer to it)
+// (the TMA maps and every other kernel refer to it); on slabs the fused
+// sweeps leave the halo rows stale, so one row is exchanged for the residual
 int smooth_end(wd_ctx* ctx, int l, cudaStream_t st) {
     for (Part& P : ctx->parts) {
         Level& F = P.lev[l];
@@ -620,6 +621,7 @@ int smooth_end(wd_ctx* ctx, int l, cudaStream_t st) {
             F.lam = F.raw[1];
         }
     }
+    if (fused_level(ctx, l)) RC(exchange(ctx, l, ARR_LAM, 1, st));
     return WD_OK;
 }
 
@@ -637,6 +639,7 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st) {
         launch_restrict(F.L, target(C), F.M, F.r, C.f, F.nkept == F.L.n3, st);
     }
     if (l + 1 == ctx->gather) RC(gather_rows(ctx, l + 1, ARR_F, st));
+    else if (fused_level(ctx, l + 1)) RC(exchange(ctx, l + 1, ARR_F, 1, st));   // halo row of f_c
     for (Part& P : ctx->parts) CK(cudaMemsetAsync(P.lev[l + 1].lam, 0, sizeof(double) * P.lev[l + 1].L.NT, st));
     CKL();
     RC(vcycle_level(ctx, l + 1, st));
@@ -1292,6 +1295,9 @@ int wd_vcycle(wd_ctx* ctx, double* lambda, const double* f, double* rel_res_out,
         launch_nat2int(P.lev[0].L, nat_nodes(ctx, P, sl.d), P.lev[0].lam, true, st);
     }
     CKL();
+    // the caller's halo rows need not be current (outputs cover owned rows)
+    RC(exchange(ctx, 0, ARR_F, 2, st));
+    RC(exchange(ctx, 0, ARR_LAM, 2, st));
     RC(run_vcycle(ctx, st));
     if (rel_res_out) {
         RC(residual_sq(ctx, 0, st));
@@ -1325,6 +1331,9 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
         else CK(cudaMemsetAsync(F.lam, 0, sizeof(double) * F.L.NT, st));
     }
     CKL();
+    // the caller's halo rows need not be current (outputs cover owned rows)
+    RC(exchange(ctx, 0, ARR_F, 2, st));
+    RC(exchange(ctx, 0, ARR_LAM, 2, st));
     wd_report R;
     memset(&R, 0, sizeof R);
     R.nlevels = ctx->nlev;

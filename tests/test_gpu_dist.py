@@ -21,9 +21,9 @@ def wd():
     return m
 
 
-def _ctx(wd, p, nranks, gather):
+def _ctx(wd, p, nranks, gather, smoother="fused"):
     opt = wd.default_options(coarsest_max_free=200, nranks=nranks, rank=-1 if nranks > 1 else 0,
-                             gather_below_nodes=gather)
+                             gather_below_nodes=gather, smoother=smoother)
     return wd.wd_assemble(p.X, p.Y, p.Z, p.a, opt)
 
 
@@ -35,11 +35,15 @@ PROBLEMS = {
 
 
 @pytest.mark.parametrize("name", list(PROBLEMS))
-@pytest.mark.parametrize("nranks,gather", [(2, 10 ** 9), (3, 1000), (4, 1000), (5, 50000)])
-def test_virtual_ranks_bitwise(wd, name, nranks, gather):
+@pytest.mark.parametrize("nranks,gather,smoother", [(2, 10 ** 9, "fused"), (3, 1000, "fused"),
+                                                    (4, 1000, "fused"), (5, 50000, "fused"),
+                                                    (3, 1000, "phased")])
+def test_virtual_ranks_bitwise(wd, name, nranks, gather, smoother):
+    """Fused sweeps on slabs: one 2-row exchange per sweep, halo row recomputed;
+    phased: exchanges after colours 1 and 3.  Both against one part (fused)."""
     p = PROBLEMS[name]()
     ref = _ctx(wd, p, 1, 0)
-    ctx = _ctx(wd, p, nranks, gather)
+    ctx = _ctx(wd, p, nranks, gather, smoother)
     assert ctx.num_levels() == ref.num_levels()
     gl = wd.wd_gather_level(ctx)
     assert gl >= 1
