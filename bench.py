@@ -45,6 +45,21 @@ GS_BYTES = {"fused": (136, 1, "gs_fused_kernel"), "phased": (66, 4, "gs_phase_ke
 CPU_CROP = 200                            # oracle sample: 200x200x15 elements of the workload
 
 
+def vcycle_hbm(levels, ms, peak, sweeps=4):
+    """Whole-V-cycle algorithmic HBM bytes over its measured
+    time: per level (free nodes F_l) `sweeps` smoother sweeps x 136 B, the
+    residual 136 B, restriction 8 B + 8 B per coarse node, prolongation
+    16 B + 8 B per coarse node (the coarsest level: dense solve, ignored)."""
+    tot = 0.0
+    for l, (n1, n2, n3) in enumerate(levels[:-1]):
+        fr = (n1 - 2) * (n2 - 2) * (n3 - 1)
+        c1, c2, c3 = levels[l + 1]
+        fc = (c1 - 2) * (c2 - 2) * (c3 - 1)
+        tot += fr * (sweeps * 136 + 136 + 8 + 16) + fc * 16
+    gbs = tot / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+    return {"bytes": tot, "achieved_GBps": gbs, "frac": gbs / peak}
+
+
 def measured_hbm_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -335,6 +350,7 @@ def run_ours(args, ws, rank, local):
                              "rhs": parts[1] / args.steps, "solve": parts[2] / args.steps,
                              "recover": parts[3] / args.steps},
             "ms_per_vcycle": vc_ms / max(vc_n, 1),
+            "vcycle_hbm": vcycle_hbm(levels, vc_ms / max(vc_n, 1), peak),
             "device_bytes": dev_bytes,
             "roofline": {"kernel": f"{gs_name} (level 0)", "bound": "hbm",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
