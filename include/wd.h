@@ -66,8 +66,13 @@ enum { WD_RULE_COUPLING_CUR = 0, WD_RULE_COUPLING_PAPER = 1, WD_RULE_VERBATIM = 
  *          shared-memory tiles (k_gs_fused.cu); on slab levels one 2-row halo
  *          exchange of lambda per sweep (default)
  *  PHASED  four launches per sweep, one per colour (k_mg.cu gs_phase_kernel);
- *          on slab levels halo rows exchanged after colours 1 and 3 */
-enum { WD_SMOOTH_FUSED = 0, WD_SMOOTH_PHASED = 1 };
+ *          on slab levels halo rows exchanged after colours 1 and 3
+ * and a different smoother (north_star "vertical-column line
+ * relaxation parallel over (i,j)"):
+ *  LINE    the same colour groups and order, each free column solved exactly
+ *          (tridiagonal in k, Thomas algorithm) given the latest values of the
+ *          other columns; four launches per sweep (k_mg.cu line_phase_kernel) */
+enum { WD_SMOOTH_FUSED = 0, WD_SMOOTH_PHASED = 1, WD_SMOOTH_LINE = 2 };
 
 typedef struct wd_ctx wd_ctx;
 

@@ -58,6 +58,7 @@ def lib():
         for name in ("orc_mg_gs", "orc_mg_apply", "orc_mg_restrict", "orc_mg_prolong"):
             getattr(L, name).argtypes = [C.c_void_p, C.c_int, _dp, _dp]
         L.orc_mg_coarse_solve.argtypes = [C.c_void_p, _dp, _dp]
+        L.orc_mg_set_smoother.argtypes = [C.c_void_p, C.c_int]
         L.orc_mg_vcycle.argtypes = [C.c_void_p, _dp, _dp]
         L.orc_mg_solve.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, _dp, _dp, _ip, _dp]
         L.orc_validate_mesh.restype = C.c_longlong
@@ -186,6 +187,18 @@ def residual(K, x, f):
     return r, nrm
 
 
+def line_sweep(K, x, f):
+    """One vertical line-relaxation sweep (orc_line_sweep)."""
+    x = _f64(x).copy()
+    K = _f64(K)
+    n3, n2, n1 = x.shape
+    lib().orc_line_sweep(_d(K), n1, n2, n3, _d(x), _d(_f64(f)))
+    return x
+
+
+SMOOTHERS = {"gs": 0, "line": 1}
+
+
 def gs_sweep(K, x, f):
     n3, n2, n1, _ = K.shape
     x = _f64(x).copy()
@@ -229,7 +242,7 @@ class MG:
     """Oracle multigrid hierarchy on one mesh."""
 
     def __init__(self, X, Y, Z, a, rule="coupling_cur", coarsest_max_free=4096, pre=2,
-                 post=2):
+                 post=2, smoother="gs"):
         self._keep = [_f64(X), _f64(Y), _f64(Z)]
         n3, n2, n1 = X.shape
         err = C.c_int(0)
@@ -239,6 +252,7 @@ class MG:
                                 int(coarsest_max_free), int(pre), int(post), C.byref(err))
         if not self.h:
             raise RuntimeError(f"orc_mg_setup failed, err={err.value}")
+        L.orc_mg_set_smoother(self.h, SMOOTHERS[smoother])
         self.nlev = L.orc_mg_nlevels(self.h)
         self.coarse_direct = bool(L.orc_mg_coarse_direct(self.h))
         self.dims = []
@@ -268,6 +282,7 @@ class MG:
         return np.ctypeslib.as_array(p, shape=(n3, n2, n1, 27)).copy()
 
     def gs(self, l, x, f):
+        """One sweep of the hierarchy's smoother (point GS or line relaxation)."""
         x = _f64(x).copy()
         lib().orc_mg_gs(self.h, l, _d(x), _d(_f64(f)))
         return x

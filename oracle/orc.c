@@ -444,6 +444,67 @@ void orc_gs_sweep(const double* K, int n1, int n2, int n3, double* x, const doub
     }
 }
 
+/* Vertical line relaxation (BASELINE north_star "vertical-
+ * column line relaxation parallel over (i,j)"): the colour groups and group
+ * order of the point smoother above (reading C7), but each free
+ * column c of a group is solved exactly for its free unknowns k = 0..n3-2
+ * given the latest values of every other column:
+ *     T_c x_c = f_c - sum_{q not in column c} K_cq x_q,
+ * T_c the column's own block, tridiagonal in k (couplings dz = -1, 0, +1;
+ * the top neighbour is Dirichlet, x = 0).  T_c is a principal submatrix of
+ * the SPD K_FF, so the Thomas algorithm (no pivoting) is stable.  Written out
+ * as the textbook recurrences:
+ *     c'_0 = c_0 / b_0,  d'_0 = r_0 / b_0,
+ *     m_k = b_k - a_k c'_{k-1},  c'_k = c_k / m_k,  d'_k = (r_k - a_k d'_{k-1}) / m_k,
+ *     x_{top} = d'_{top},  x_k = d'_k - c'_k x_{k+1}. */
+void orc_line_sweep(const double* K, int n1, int n2, int n3, double* x, const double* f) {
+    static const int colour[4][2] = {{0, 0}, {1, 0}, {0, 1}, {1, 1}};
+    const int m = n3 - 1;   /* free unknowns per column */
+    for (int c = 0; c < 4; c++) {
+        int ci = colour[c][0], cj = colour[c][1];
+#pragma omp parallel for schedule(static)
+        for (int j = 1; j < n2 - 1; j++) {
+            if ((j & 1) != cj) continue;
+            double* cp = (double*)malloc(sizeof(double) * (size_t)m);
+            double* dp = (double*)malloc(sizeof(double) * (size_t)m);
+            for (int i = 1; i < n1 - 1; i++) {
+                if ((i & 1) != ci) continue;
+                for (int k = 0; k < m; k++) {
+                    i64 p = nid(n1, n2, i, j, k);
+                    /* r_k = f_k - (off-column part of row p) */
+                    double s = 0.0;
+                    for (int dz = -1; dz <= 1; dz++) {
+                        int kk = k + dz;
+                        if (kk < 0 || kk >= n3) continue;
+                        for (int dy = -1; dy <= 1; dy++)
+                            for (int dx = -1; dx <= 1; dx++) {
+                                if (dx == 0 && dy == 0) continue;
+                                s += K[p * 27 + o27(dx, dy, dz)] * x[nid(n1, n2, i + dx, j + dy, kk)];
+                            }
+                    }
+                    double r = f[p] - s;
+                    double a = k > 0 ? K[p * 27 + o27(0, 0, -1)] : 0.0;
+                    double b = K[p * 27 + o27(0, 0, 0)];
+                    double cc = k < m - 1 ? K[p * 27 + o27(0, 0, 1)] : 0.0;
+                    if (k == 0) {
+                        cp[0] = cc / b;
+                        dp[0] = r / b;
+                    } else {
+                        double mk = b - a * cp[k - 1];
+                        cp[k] = cc / mk;
+                        dp[k] = (r - a * dp[k - 1]) / mk;
+                    }
+                }
+                x[nid(n1, n2, i, j, m - 1)] = dp[m - 1];
+                for (int k = m - 2; k >= 0; k--)
+                    x[nid(n1, n2, i, j, k)] = dp[k] - cp[k] * x[nid(n1, n2, i, j, k + 1)];
+            }
+            free(cp);
+            free(dp);
+        }
+    }
+}
+
 /* ------------------------------------------------------------------ */
 /* coarsening plan, readings C1-C5 of DESIGN.md             */
 /* ------------------------------------------------------------------ */
@@ -541,6 +602,7 @@ typedef struct {
     int cmax;
     int coarse_direct;    /* 1: dense Cholesky; 0: fallback GS sweeps (C8) */
     int coarse_iters;
+    int smoother;         /* 0: point GS, 1: vertical line relaxation (f1) */
     int nf;               /* free unknowns on the coarsest level */
     i64* fidx;            /* free node index list (natural order) */
     double* chol;         /* nf x nf lower factor */
@@ -550,6 +612,15 @@ typedef struct {
 
 static i64 level_N(const orc_level* l) { return (i64)l->n1 * l->n2 * l->n3; }
 static i64 level_free(int n1, int n2, int n3) { return (i64)(n1 - 2) * (n2 - 2) * (n3 - 1); }
+
+/* one sweep of the hierarchy's smoother on level l */
+static void mg_smooth(const orc_mg* mg, const orc_level* l, double* x, const double* f) {
+    if (mg->smoother == 1) orc_line_sweep(l->K, l->n1, l->n2, l->n3, x, f);
+    else orc_gs_sweep(l->K, l->n1, l->n2, l->n3, x, f);
+}
+
+/* select the smoother (0 point GS, 1 vertical line relaxation) */
+void orc_mg_set_smoother(orc_mg* mg, int smoother) { mg->smoother = smoother; }
 
 /* parents of fine index t along direction d of level l: returns count (1|2) */
 static inline int parents(const orc_level* l, int d, int t, int* pc, double* pw) {
@@ -771,6 +842,7 @@ orc_mg* orc_mg_setup(const double* X, const double* Y, const double* Z, int n1, 
     orc_mg* mg = (orc_mg*)calloc(1, sizeof(orc_mg));
     mg->pre = pre; mg->post = post; mg->rule = rule; mg->cmax = cmax;
     mg->coarse_iters = 50;
+    mg->smoother = 0;
     double c[3] = {1.0 / (a1 * a1), 1.0 / (a2 * a2), 1.0 / (a3 * a3)};
     alloc_level(&mg->L[0], n1, n2, n3);
     mg->nlev = 1;
@@ -837,7 +909,7 @@ int orc_mg_plan(const orc_mg* mg, int l, int* hflag, int* kept) {
     return mg->L[l].nkept;
 }
 void orc_mg_gs(orc_mg* mg, int l, double* x, const double* f) {
-    orc_gs_sweep(mg->L[l].K, mg->L[l].n1, mg->L[l].n2, mg->L[l].n3, x, f);
+    mg_smooth(mg, &mg->L[l], x, f);
 }
 void orc_mg_apply(orc_mg* mg, int l, const double* x, double* y) {
     orc_apply(mg->L[l].K, mg->L[l].n1, mg->L[l].n2, mg->L[l].n3, x, y);
@@ -855,7 +927,7 @@ void orc_mg_coarse_solve(orc_mg* mg, const double* f, double* x) {
         coarse_solve(mg, f, x);
     } else {
         memset(x, 0, sizeof(double) * level_N(l));
-        for (int s = 0; s < mg->coarse_iters; s++) orc_gs_sweep(l->K, l->n1, l->n2, l->n3, x, f);
+        for (int s = 0; s < mg->coarse_iters; s++) mg_smooth(mg, l, x, f);
     }
 }
 
@@ -865,14 +937,14 @@ void orc_mg_coarse_solve(orc_mg* mg, const double* f, double* x) {
 static void vcycle_rec(orc_mg* mg, int l, double* x, const double* f) {
     orc_level* L = &mg->L[l];
     if (l == mg->nlev - 1) { orc_mg_coarse_solve(mg, f, x); return; }
-    for (int s = 0; s < mg->pre; s++) orc_gs_sweep(L->K, L->n1, L->n2, L->n3, x, f);
+    for (int s = 0; s < mg->pre; s++) mg_smooth(mg, L, x, f);
     orc_residual(L->K, L->n1, L->n2, L->n3, x, f, L->r);
     orc_level* C = &mg->L[l + 1];
     restrict_(L, C, L->r, C->f);
     memset(C->x, 0, sizeof(double) * level_N(C));
     vcycle_rec(mg, l + 1, C->x, C->f);
     prolong_(L, C, C->x, x);
-    for (int s = 0; s < mg->post; s++) orc_gs_sweep(L->K, L->n1, L->n2, L->n3, x, f);
+    for (int s = 0; s < mg->post; s++) mg_smooth(mg, L, x, f);
 }
 
 void orc_mg_vcycle(orc_mg* mg, double* x, const double* f) { vcycle_rec(mg, 0, x, f); }

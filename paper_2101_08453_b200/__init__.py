@@ -27,7 +27,7 @@ _lib = C.CDLL(LIB_PATH)
 WD_OK, WD_E_INVAL, WD_E_MESH, WD_E_NOCONV, WD_E_DIVERGED, WD_E_NONFINITE, WD_E_CUDA, \
     WD_E_NCCL, WD_E_OOM, WD_E_INTERNAL = range(10)
 RULES = {"coupling_cur": 0, "coupling_paper": 1, "verbatim": 2, "full": 3}
-SMOOTHERS = {"fused": 0, "phased": 1}
+SMOOTHERS = {"fused": 0, "phased": 1, "line": 2}
 ERRNAMES = {1: "WD_E_INVAL", 2: "WD_E_MESH", 3: "WD_E_NOCONV", 4: "WD_E_DIVERGED",
             5: "WD_E_NONFINITE", 6: "WD_E_CUDA", 7: "WD_E_NCCL", 8: "WD_E_OOM",
             9: "WD_E_INTERNAL"}

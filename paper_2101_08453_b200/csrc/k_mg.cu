@@ -110,6 +110,94 @@ gs_phase_kernel(LevDev L, const double* __restrict__ K, double* lam,
     }
 }
 
+// One colour phase of vertical line relaxation: every free
+// column of the colour is solved exactly for its planes 0..n3-2 given the
+// current values of the 8 neighbouring columns (columns of one colour are not
+// neighbours, so the phase is order-independent):  T x = f - (off-column
+// part of K x), T tridiagonal with a_k = K(k, k-1) (slot 9 stored at k-1),
+// b_k = K(k, k), c_k = K(k, k+1) (slot 9 at k; the top plane is Dirichlet).
+// Thomas algorithm: forward elimination bottom-up (c'_k into cpb, d'_k into
+// dpb at the node's own offset), back substitution top-down into lam.
+__global__ void __launch_bounds__(GS_BLK)
+line_phase_kernel(LevDev L, const double* __restrict__ K, double* lam,
+                  const double* __restrict__ f, double* __restrict__ cpb, double* __restrict__ dpb,
+                  int ci, int cj) {
+    const int a = blockIdx.x * GS_BLK + threadIdx.x;
+    const int i = 2 * a + ci;
+    const int j = L.own0 + ((cj - (L.own0 + L.jg0)) & 1) + 2 * (int)blockIdx.y;
+    if (i < 1 || i > L.n1 - 2 || !row_free(L, j)) return;
+    i64 co[9];
+    column_offsets(L, ci, co);
+    const i64 own = loff(L, i, j, 0);
+    const i64 NT = L.NT;
+    double xm[9], x0[9], xp[9];
+#pragma unroll
+    for (int c = 0; c < 9; c++) {
+        xm[c] = 0.0;
+        x0[c] = c == 4 ? 0.0 : ldg(lam + own + co[c]);
+        xp[c] = c == 4 ? 0.0 : ldg(lam + own + L.sk + co[c]);
+    }
+    const int m = L.n3 - 1;   // free planes
+    double cprev = 0.0, dprev = 0.0;
+    for (int k = 0; k < m; k++) {
+        const i64 base = own + (i64)k * L.sk;
+        double s = 0.0;
+        // forward couplings except the own column's (slot 9 = (0,0,1))
+#pragma unroll
+        for (int sl = 1; sl < 14; sl++) {
+            const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+            if (dx == 0 && dy == 0) continue;
+            s = fma(ldg(K + sl * NT + base), dz ? xp[cidx(dx, dy)] : x0[cidx(dx, dy)], s);
+        }
+        // backward couplings except the own column's
+#pragma unroll
+        for (int sl = 1; sl < 14; sl++) {
+            const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+            if (dx == 0 && dy == 0) continue;
+            if (dz) {
+                if (k > 0) s = fma(ldg(K + sl * NT + base - L.sk + co[cidx(-dx, -dy)]), xm[cidx(-dx, -dy)], s);
+            } else {
+                s = fma(ldg(K + sl * NT + base + co[cidx(-dx, -dy)]), x0[cidx(-dx, -dy)], s);
+            }
+        }
+        const double r = ldg(f + base) - s;
+        const double b = ldg(K + base);
+        const double cc = k < m - 1 ? ldg(K + 9 * NT + base) : 0.0;
+        double cp, dp;
+        if (k == 0) {
+            cp = cc / b;
+            dp = r / b;
+        } else {
+            const double ak = ldg(K + 9 * NT + base - L.sk);
+            const double mk = b - ak * cprev;
+            cp = cc / mk;
+            dp = (r - ak * dprev) / mk;
+        }
+        cpb[base] = cp;
+        dpb[base] = dp;
+        cprev = cp;
+        dprev = dp;
+#pragma unroll
+        for (int c = 0; c < 9; c++) {
+            xm[c] = x0[c];
+            x0[c] = xp[c];
+        }
+        if (k + 2 <= L.n3 - 1) {
+            const i64 nb = base + 2 * L.sk;
+#pragma unroll
+            for (int c = 0; c < 9; c++) xp[c] = c == 4 ? 0.0 : ldg(lam + nb + co[c]);
+        }
+    }
+    // back substitution, top-down
+    double xn = dprev;
+    lam[own + (i64)(m - 1) * L.sk] = xn;
+    for (int k = m - 2; k >= 0; k--) {
+        const i64 base = own + (i64)k * L.sk;
+        xn = dpb[base] - cpb[base] * xn;
+        lam[base] = xn;
+    }
+}
+
 // deterministic block reduction (warp shuffle tree + fixed-order smem)
 __device__ __forceinline__ double block_sum(double v) {
     __shared__ double ws[32];
@@ -541,6 +629,15 @@ void launch_gs_phase(const LevDev& L, const double* coef, double* lam, const dou
     dim3 grid((half + GS_BLK - 1) / GS_BLK, (L.own1 - L.own0 + 2) / 2);
     g_launches += 1;
     gs_phase_kernel<<<grid, GS_BLK, 0, st>>>(L, coef, lam, f, colour[c][0], colour[c][1]);
+}
+
+void launch_line_phase(const LevDev& L, const double* coef, double* lam, const double* f,
+                       double* cpb, double* dpb, int c, cudaStream_t st) {
+    static const int colour[4][2] = {{0, 0}, {1, 0}, {0, 1}, {1, 1}};
+    const int half = (L.n1 + 1) / 2;
+    dim3 grid((half + GS_BLK - 1) / GS_BLK, (L.own1 - L.own0 + 2) / 2);
+    g_launches += 1;
+    line_phase_kernel<<<grid, GS_BLK, 0, st>>>(L, coef, lam, f, cpb, dpb, colour[c][0], colour[c][1]);
 }
 
 void launch_gs_sweep(const LevDev& L, const double* coef, double* lam, const double* f,

@@ -579,14 +579,16 @@ int coarse_solve(wd_ctx* ctx, cudaStream_t st) {
 
 // does level l use the fused one-pass sweep (k_gs_fused.cu)?
 bool fused_level(const wd_ctx* ctx, int l) { return ctx->opt.smoother == WD_SMOOTH_FUSED; }
+bool line_level(const wd_ctx* ctx, int l) { return ctx->opt.smoother == WD_SMOOTH_LINE; }
 
 // one smoothing sweep on level l.
 //  * fused: lam -> lam2 in one launch, then the two buffers swap roles (the
 //    caller restores the canonical buffer with smooth_end); on slabs the two
 //    halo rows of the input iterate are exchanged first (the sweep recomputes
 //    the nearest halo row as tile halo and writes owned rows only);
-//  * phased: 4 colour phases in place; on slabs the boundary rows are
-//    exchanged after phase 1 (even rows final) and phase 3 (odd rows final)
+//  * phased / line relaxation: 4 colour phases in place; on slabs the boundary
+//    rows are exchanged after phase 1 (even rows final) and phase 3 (odd rows
+//    final)
 int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st) {
     if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns], st, cudaEventRecordExternal));
     if (fused_level(ctx, l)) {
@@ -600,7 +602,8 @@ int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st) {
         for (int c = 0; c < 4; c++) {
             for (Part& P : ctx->parts) {
                 Level& F = P.lev[l];
-                launch_gs_phase(F.L, F.coef, F.lam, F.f, c, st);
+                if (line_level(ctx, l)) launch_line_phase(F.L, F.coef, F.lam, F.f, F.lam2, F.r, c, st);
+                else launch_gs_phase(F.L, F.coef, F.lam, F.f, c, st);
             }
             if (c == 1 || c == 3) RC(exchange(ctx, l, ARR_LAM, 1, st));
         }
@@ -1237,7 +1240,7 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
         return fail(WD_E_INVAL, "penalty constants must be positive and finite");
     if (opt && (opt->pre_smooth < 0 || opt->post_smooth < 0 || opt->max_cycles < 0 ||
                 opt->coarsen_rule < 0 || opt->coarsen_rule > 3 || opt->coarse_iters < 0 ||
-                opt->smoother < 0 || opt->smoother > 1))
+                opt->smoother < 0 || opt->smoother > 2))
         return fail(WD_E_INVAL, "invalid options");
     if (opt && opt->coarsest_max_free > 8192)
         return fail(WD_E_INVAL, "coarsest_max_free %d > 8192 (dense inverse)", opt->coarsest_max_free);

@@ -106,6 +106,10 @@ void launch_gs_sweep(const LevDev& L, const double* coef, double* lam, const dou
                      cudaStream_t st);
 void launch_gs_phase(const LevDev& L, const double* coef, double* lam, const double* f, int c,
                      cudaStream_t st);
+// colour phase c of vertical line relaxation; cpb/dpb: two
+// level-sized scratch arrays for the Thomas recurrences
+void launch_line_phase(const LevDev& L, const double* coef, double* lam, const double* f,
+                       double* cpb, double* dpb, int c, cudaStream_t st);
 void launch_sum_ordered(const double* v, int n, double* out, cudaStream_t st);
 // y = K x (f == NULL) or y = f - K x; optional block partials of sum y^2
 int launch_apply(const LevDev& L, const double* coef, const double* x, const double* f,

@@ -171,3 +171,28 @@ def gs_dense(A, f, x, order):
     out = x.ravel().copy()
     out[order] = xn
     return out.reshape(x.shape)
+
+
+def line_dense(A, f, x, shape):
+    """One block Gauss-Seidel sweep whose blocks are the free vertical columns,
+    in the smoother's colour order (0,0),(1,0),(0,1),(1,1), each block solved
+    exactly with numpy (dense) given the latest values of all other nodes:
+    x_c <- A_cc^{-1} (f_c - sum_{q not in c} A_cq x_q).  Independent of the
+    oracle's Thomas recurrences."""
+    n3, n2, n1 = shape
+    m = free_mask(shape).ravel()
+    xv = x.ravel().copy()
+    fv = f.ravel()
+    for (ci, cj) in [(0, 0), (1, 0), (0, 1), (1, 1)]:
+        for j in range(1, n2 - 1):
+            if j % 2 != cj:
+                continue
+            for i in range(1, n1 - 1):
+                if i % 2 != ci:
+                    continue
+                idx = np.array([(k * n2 + j) * n1 + i for k in range(n3 - 1)])
+                rest = m.copy()
+                rest[idx] = False
+                r = fv[idx] - A[np.ix_(idx, np.flatnonzero(rest))] @ xv[rest]
+                xv[idx] = np.linalg.solve(A[np.ix_(idx, idx)], r)
+    return xv.reshape(shape)

@@ -37,12 +37,12 @@ PROBLEMS = {
 @pytest.mark.parametrize("name", list(PROBLEMS))
 @pytest.mark.parametrize("nranks,gather,smoother", [(2, 10 ** 9, "fused"), (3, 1000, "fused"),
                                                     (4, 1000, "fused"), (5, 50000, "fused"),
-                                                    (3, 1000, "phased")])
+                                                    (3, 1000, "phased"), (3, 1000, "line")])
 def test_virtual_ranks_bitwise(wd, name, nranks, gather, smoother):
     """Fused sweeps on slabs: one 2-row exchange per sweep, halo row recomputed;
     phased: exchanges after colours 1 and 3.  Both against one part (fused)."""
     p = PROBLEMS[name]()
-    ref = _ctx(wd, p, 1, 0)
+    ref = _ctx(wd, p, 1, 0, "line" if smoother == "line" else "fused")
     ctx = _ctx(wd, p, nranks, gather, smoother)
     assert ctx.num_levels() == ref.num_levels()
     gl = wd.wd_gather_level(ctx)

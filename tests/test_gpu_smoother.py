@@ -120,3 +120,45 @@ def test_galerkin_unrolled_path_bitwise(wd, name, monkeypatch):
         assert torch.equal(a, b), (name, l, (a - b).abs().max().item())
     fast.close()
     gen.close()
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "ragged_a", "thin"])
+def test_line_relaxation_matches_oracle(wd, name):
+    """Vertical line relaxation: one GPU sweep on every level
+    against the oracle's Thomas-algorithm sweep (<= 1e-11 relative max)."""
+    p = GRIDS[name]()
+    X, Y, Z, u0 = p.numpy()
+    g = p.to(DEV)
+    ctx = wd.wd_assemble(g.X, g.Y, g.Z, p.a, wd.default_options(coarsest_max_free=60,
+                                                                 smoother="line"))
+    mg = oracle.MG(X, Y, Z, p.a, coarsest_max_free=60, smoother="line")
+    assert ctx.num_levels() == mg.nlev
+    rng = np.random.default_rng(9)
+    for l in range(mg.nlev):
+        s = mg.shape(l)
+        x = rng.uniform(-1, 1, s) * free_mask(s)
+        f = rng.uniform(-1, 1, s) * free_mask(s)
+        got = wd.wd_smooth(ctx, l, torch.as_tensor(x, device=DEV), torch.as_tensor(f, device=DEV),
+                           sweeps=1).cpu().numpy()
+        ref = mg.gs(l, x, f)
+        assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max(), (name, l)
+    ctx.close()
+
+
+@pytest.mark.parametrize("name", ["small", "ragged_a"])
+def test_line_relaxation_solve_parity(wd, name):
+    """Solves with the line smoother on both sides: lambda within 1e-8
+    relative l2 at rel. residual 1e-10, convergence factor within 10 %."""
+    p = GRIDS[name]()
+    X, Y, Z, u0 = p.numpy()
+    g = p.to(DEV)
+    ctx = wd.wd_assemble(g.X, g.Y, g.Z, p.a, wd.default_options(coarsest_max_free=60,
+                                                                 smoother="line"))
+    mg = oracle.MG(X, Y, Z, p.a, coarsest_max_free=60, smoother="line")
+    f = oracle.rhs(X, Y, Z, u0)
+    lam, rep = wd.wd_solve(ctx, torch.as_tensor(f, device=DEV), rel_tol=1e-10)
+    lo, ro = mg.solve(f, tol=1e-10)
+    lam = lam.cpu().numpy()
+    assert np.linalg.norm(lam - lo) <= 1e-8 * np.linalg.norm(lo)
+    assert abs(rep["rate"] - ro["rate"]) <= 0.1 * ro["rate"], (rep["rate"], ro["rate"])
+    ctx.close()

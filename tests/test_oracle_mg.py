@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 import synth
-from brute import (fast_diag_solve, free_mask, gs_dense, gs_order, prolong_dense)
+from brute import (fast_diag_solve, free_mask, gs_dense, gs_order, line_dense, prolong_dense)
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
 
@@ -184,6 +184,66 @@ def test_gs_single_free_node_exact():
     assert x[0, 1, 1] == 3.0 / K[0, 1, 1, 13]
 
 
+def test_line_sweep_is_dense_block_gs():
+    """Vertical line relaxation == block GS over free columns
+    in the colour order, each column block solved densely (numpy), on Tiny
+    with a3 = 4; plus the fixed point and K-norm monotonicity."""
+    p = synth.tiny()
+    X, Y, Z, u0 = _np(p)
+    K = oracle.assemble(X, Y, Z, (1, 1, 4))
+    A = oracle.stencil_to_dense(K)
+    f = oracle.rhs(X, Y, Z, u0)
+    x0 = synth.random_lambda(p, 1).numpy()
+    got = oracle.line_sweep(K, x0, f)
+    want = line_dense(A, f, x0, X.shape)
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-13 * np.abs(want).max())
+    m = free_mask(X.shape).ravel()
+    xs = np.zeros(m.size)
+    xs[m] = np.linalg.solve(A[np.ix_(m, m)], f.ravel()[m])
+    xs = xs.reshape(X.shape)
+    np.testing.assert_allclose(oracle.line_sweep(K, xs, f), xs, atol=1e-12 * np.abs(xs).max())
+    x = x0
+    e_prev = np.inf
+    for _ in range(4):
+        d = (x - xs).ravel()
+        e = d @ A @ d
+        assert e <= e_prev
+        e_prev = e
+        x = oracle.line_sweep(K, x, f)
+
+
+def test_line_single_column_exact():
+    """One free column (2x2 elements in x-y): one line sweep solves K x = f
+    exactly (the column block is the whole free system)."""
+    p = synth.box(2, 2, 6, dz=np.array([1.0, 2.0, 3.0, 1.0, 2.0, 4.0]))
+    X, Y, Z, _ = _np(p)
+    K = oracle.assemble(X, Y, Z, (1, 1, 3))
+    A = oracle.stencil_to_dense(K)
+    m = free_mask(X.shape).ravel()
+    rng = np.random.default_rng(3)
+    f = rng.standard_normal(X.shape) * free_mask(X.shape)
+    x = oracle.line_sweep(K, np.zeros(X.shape), f)
+    xs = np.linalg.solve(A[np.ix_(m, m)], f.ravel()[m])
+    np.testing.assert_allclose(x.ravel()[m], xs, rtol=0, atol=1e-13 * np.abs(xs).max())
+
+
+@pytest.mark.parametrize("a3", [1, 10])
+def test_mg_line_smoother_matches_dense_direct_tiny(a3):
+    """The V-cycle with line relaxation converges to the dense direct
+    solution (1e-8 relative l2 at rel. residual 1e-10)."""
+    p = synth.tiny()
+    X, Y, Z, u0 = _np(p)
+    a = (1, 1, a3)
+    f = oracle.rhs(X, Y, Z, u0)
+    mg = oracle.MG(X, Y, Z, a, coarsest_max_free=100, smoother="line")
+    lam, rep = mg.solve(f, tol=1e-10)
+    assert rep["status"] == 0 and rep["cycles"] <= 30
+    A = oracle.stencil_to_dense(oracle.assemble(X, Y, Z, a))
+    m = free_mask(X.shape).ravel()
+    xs = np.linalg.solve(A[np.ix_(m, m)], f.ravel()[m])
+    assert np.linalg.norm(lam.ravel()[m] - xs) <= 1e-8 * np.linalg.norm(xs)
+
+
 # --------------------------------------------------------------- cycles
 def test_two_grid_cycle_dense():
     """Two-level V-cycle = S_post o (I + P Kc^{-1} P^T (f - K .)) o S_pre with
@@ -294,5 +354,9 @@ def test_rate_semicoarsening_hill_anchor(a3):
     rng = np.random.default_rng(0)
     f = rng.standard_normal(X.shape) * free_mask(X.shape)
     mg = oracle.MG(X, Y, Z, p.a)
+    _, rep = mg.solve(f, tol=1e-30, max_cycles=10)
+    assert rep["rate"] <= 0.35, rep["rate"]
+    # the f1 line-relaxation smoother meets the same anchor (measured 0.22 / 0.11 / 0.28)
+    mg = oracle.MG(X, Y, Z, p.a, smoother="line")
     _, rep = mg.solve(f, tol=1e-30, max_cycles=10)
     assert rep["rate"] <= 0.35, rep["rate"]
