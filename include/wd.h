@@ -216,6 +216,51 @@ void wd_profile_reset(wd_ctx* ctx);
 /* Cumulative number of kernel launches executed by this library in this
  * process (a CUDA-graph replay counts its kernel nodes). */
 long long wd_launch_count(void);
+/* ---- steps either side of the solver ---------------- */
+
+/* Terrain-following mesh from a terrain array ("terrain-following
+ * grid"; the domain-top reading C13 of DESIGN.md):
+ *   X(i,j,k) = x0 + i dx,  Y(i,j,k) = y0 + j dy,
+ *   Z(i,j,k) = zs(i,j) + zeta[k] (H - zs(i,j)) / zeta[n3-1].
+ * zs: terrain [n2][n1] (device or host); zeta: n3 level heights, HOST array,
+ * zeta[0] = 0, strictly increasing; H: the flat domain top; X, Y, Z: node
+ * arrays [n3][n2][n1] (written; device or host).  Every cell of the result is
+ * valid (detJ > 0) when H > zs everywhere.  Synchronous.  Errors: WD_E_INVAL
+ * (NULL, n < 2, dx/dy <= 0, non-finite, zeta not increasing from 0),
+ * WD_E_MESH (H <= zs at some column; the message names the first one). */
+int wd_build_mesh(const double* zs, int n1, int n2, double x0, double y0, double dx, double dy,
+                  const double* zeta, int n3, double H, double* X, double* Y, double* Z,
+                  void* stream);
+
+/* Interpolation of a coarse (WRF-like) wind to the element centres of a mesh
+ * (the fire grid's initial wind u0 comes from the
+ * atmospheric model).  uc: [3][nzc][nyc][nxc] (u, v, w) on the horizontal grid
+ * (xc0 + a DXc, yc0 + b DYc) at heights above ground hc[0..nzc-1] (HOST
+ * array, strictly increasing); X, Y, Z: node arrays [n3][n2][n1]; u0: element
+ * array [3][n3-1][n2-1][n1-1] (written).  Per element: centre = mean of its 8
+ * nodes, height above ground = centre Z - mean of its column's 4 bottom-node
+ * Z; value = trilinear interpolant in (x, y, height), each coordinate clamped
+ * to the coarse grid.  Synchronous.  Errors: WD_E_INVAL. */
+int wd_interp_wind(const double* uc, int nxc, int nyc, int nzc, double xc0, double yc0,
+                   double DXc, double DYc, const double* hc, const double* X, const double* Y,
+                   const double* Z, int n1, int n2, int n3, double* u0, void* stream);
+
+/* Mass-consistency diagnostics of a wind u (element array) on the context's
+ * mesh (Eq. (1) "div u = 0"; reading C12): the one-point weak divergence
+ * D1(u)_mu = sum_e 8 detJ_e(0) grad mu(0) . u_e over the free nodes mu;
+ * out[0] = its l2 norm, out[1] = its max abs (host array).  For the
+ * recovered wind D1(u) = (K1 - K) lambda + (K lambda - f) (C12): not zero,
+ * but the projection lowers it below D1(u0) = -f.  Synchronous. */
+int wd_mass_consistency(wd_ctx* ctx, const double* u, double out[2], void* stream);
+
+/* One model time step with the persistent hierarchy: f = RHS(u0),
+ * lambda = solve (warm-started from the caller's lambda when warm != 0, from
+ * zero otherwise) to rel_tol, u = u0 + A^-1 grad lambda.  lambda is in/out
+ * (node array), u out (element array); rep nullable.  Returns wd_solve's
+ * status (the wind is recovered also for WD_E_NOCONV). */
+int wd_downscale_step(wd_ctx* ctx, const double* u0, double* lambda, int warm, double rel_tol,
+                      double* u, wd_report* rep, void* stream);
+
 /* Time one internal kernel (or step) on the context's own buffers with CUDA
  * events: which = 0 GS sweep (the context's smoother), 1 residual apply,
  * 2 restrict (level -> level+1), 3 prolong, 4 V-cycle (level 0), 5 residual

@@ -62,6 +62,12 @@ def lib():
         L.orc_mg_vcycle.argtypes = [C.c_void_p, _dp, _dp]
         L.orc_mg_solve.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, _dp, _dp, _ip, _dp]
         L.orc_validate_mesh.restype = C.c_longlong
+        L.orc_build_mesh.restype = C.c_longlong
+        L.orc_build_mesh.argtypes = [_dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                     C.c_double, _dp, C.c_int, C.c_double, _dp, _dp, _dp]
+        L.orc_interp_wind.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                      C.c_double, C.c_double, _dp, _dp, _dp, _dp, C.c_int, C.c_int,
+                                      C.c_int, _dp]
         L.orc_residual.restype = C.c_double
         L.orc_norm2.restype = C.c_double
         L.orc_plan_level.argtypes = [C.c_double, _dp, C.c_int, C.c_double, C.c_double,
@@ -185,6 +191,37 @@ def residual(K, x, f):
     r = np.zeros((n3, n2, n1))
     nrm = lib().orc_residual(_d(K), n1, n2, n3, _d(_f64(x)), _d(_f64(f)), _d(r))
     return r, nrm
+
+
+def build_mesh(zs, x0, y0, dx, dy, zeta, H):
+    """Terrain-following mesh (orc_build_mesh, reading C13).
+    zs: (n2, n1); returns X, Y, Z of shape (n3, n2, n1); raises on H <= zs."""
+    zs = _f64(zs)
+    zeta = _f64(zeta)
+    n2, n1 = zs.shape
+    n3 = zeta.size
+    X, Y, Z = (np.zeros((n3, n2, n1)) for _ in range(3))
+    rc = lib().orc_build_mesh(_d(zs), n1, n2, float(x0), float(y0), float(dx), float(dy),
+                              _d(zeta), n3, float(H), _d(X), _d(Y), _d(Z))
+    if rc:
+        raise ValueError(f"domain top below the terrain at column {rc - 1}")
+    return X, Y, Z
+
+
+def interp_wind(uc, xc0, yc0, DXc, DYc, hc, X, Y, Z):
+    """Coarse wind uc (3, nzc, nyc, nxc) at heights above ground hc to element
+    centres of the mesh (orc_interp_wind)."""
+    uc = _f64(uc)
+    hc = _f64(hc)
+    _, nzc, nyc, nxc = uc.shape
+    n3, n2, n1 = X.shape
+    u0 = np.zeros((3, n3 - 1, n2 - 1, n1 - 1))
+    rc = lib().orc_interp_wind(_d(uc), nxc, nyc, nzc, float(xc0), float(yc0), float(DXc),
+                               float(DYc), _d(hc), _d(_f64(X)), _d(_f64(Y)), _d(_f64(Z)), n1, n2,
+                               n3, _d(u0))
+    if rc:
+        raise ValueError("coarse grid needs >= 2 points per direction")
+    return u0
 
 
 def line_sweep(K, x, f):

@@ -233,6 +233,100 @@ i64 orc_validate_mesh(const double* X, const double* Y, const double* Z, int n1,
 }
 
 /* ------------------------------------------------------------------ */
+/* steps either side of the path                       */
+/* ------------------------------------------------------------------ */
+
+/* Terrain-following mesh ("terrain-following grid"; the domain top
+ * reading C13 of DESIGN.md; SPEC build_mesh):
+ *   X(i,j,k) = x0 + i dx,  Y(i,j,k) = y0 + j dy,
+ *   Z(i,j,k) = zs(i,j) + zeta_k (H - zs(i,j)) / zeta_{n3-1},
+ * zs: terrain [n2][n1], zeta: n3 level heights (zeta_0 = 0, increasing), H:
+ * flat domain top.  Returns 0, or 1 + (j n1 + i) of the first column with
+ * H <= zs (no valid cell there). */
+i64 orc_build_mesh(const double* zs, int n1, int n2, double x0, double y0, double dx, double dy,
+                   const double* zeta, int n3, double H, double* X, double* Y, double* Z) {
+    for (i64 c = 0; c < (i64)n1 * n2; c++)
+        if (!(H > zs[c])) return 1 + c;
+    const double T = zeta[n3 - 1];
+    for (int k = 0; k < n3; k++)
+        for (int j = 0; j < n2; j++)
+            for (int i = 0; i < n1; i++) {
+                const i64 p = nid(n1, n2, i, j, k);
+                const double z = zs[(i64)j * n1 + i];
+                X[p] = x0 + i * dx;
+                Y[p] = y0 + j * dy;
+                Z[p] = z + zeta[k] * (H - z) / T;
+            }
+    return 0;
+}
+
+/* Coarse (WRF-like) wind to element centres (the fire
+ * grid's initial wind u0 "downscaled" from the atmospheric model's):
+ * uc [3][nzc][nyc][nxc] given on the horizontal grid (xc0 + a DXc, yc0 + b DYc)
+ * at heights above ground hc[0..nzc-1] (increasing).  For every element:
+ * centre (xe, ye, ze) = mean of its 8 nodes, height above ground
+ * he = ze - (mean of the 4 bottom nodes' Z); the value is the trilinear
+ * interpolant (bilinear in x, y; linear in he between the bracketing hc),
+ * with all three coordinates clamped to the coarse grid's extent. */
+static void bracket(double t, int n, int* i0, double* w) {
+    /* t in index units; clamp to [0, n-1]; i0 in [0, n-2], weight of i0+1 */
+    if (t <= 0.0) { *i0 = 0; *w = 0.0; return; }
+    if (t >= n - 1) { *i0 = n - 2; *w = 1.0; return; }
+    int a = (int)floor(t);
+    if (a > n - 2) a = n - 2;
+    *i0 = a;
+    *w = t - a;
+}
+
+int orc_interp_wind(const double* uc, int nxc, int nyc, int nzc, double xc0, double yc0,
+                    double DXc, double DYc, const double* hc, const double* X, const double* Y,
+                    const double* Z, int n1, int n2, int n3, double* u0) {
+    if (nxc < 2 || nyc < 2 || nzc < 2) return -1;
+    const int nx = n1 - 1, ny = n2 - 1, nz = n3 - 1;
+    const i64 ne = (i64)nx * ny * nz;
+#pragma omp parallel for schedule(static)
+    for (int k = 0; k < nz; k++)
+        for (int j = 0; j < ny; j++)
+            for (int i = 0; i < nx; i++) {
+                double xe = 0, ye = 0, ze = 0, zb = 0;
+                for (int c = 0; c < 2; c++)
+                    for (int b = 0; b < 2; b++)
+                        for (int a = 0; a < 2; a++) {
+                            const i64 p = nid(n1, n2, i + a, j + b, k + c);
+                            xe += X[p]; ye += Y[p]; ze += Z[p];
+                        }
+                for (int b = 0; b < 2; b++)
+                    for (int a = 0; a < 2; a++) zb += Z[nid(n1, n2, i + a, j + b, 0)];
+                xe /= 8.0; ye /= 8.0; ze /= 8.0; zb /= 4.0;
+                const double he = ze - zb;
+                int ia, ib, ic;
+                double wa, wb, wc;
+                bracket((xe - xc0) / DXc, nxc, &ia, &wa);
+                bracket((ye - yc0) / DYc, nyc, &ib, &wb);
+                /* vertical: find the bracketing pair of heights */
+                if (he <= hc[0]) { ic = 0; wc = 0.0; }
+                else if (he >= hc[nzc - 1]) { ic = nzc - 2; wc = 1.0; }
+                else {
+                    ic = 0;
+                    while (ic < nzc - 2 && he >= hc[ic + 1]) ic++;
+                    wc = (he - hc[ic]) / (hc[ic + 1] - hc[ic]);
+                }
+                const i64 e = ((i64)k * ny + j) * nx + i;
+                for (int m = 0; m < 3; m++) {
+                    double v = 0.0;
+                    for (int c = 0; c < 2; c++)
+                        for (int b = 0; b < 2; b++)
+                            for (int a = 0; a < 2; a++) {
+                                const double w = (a ? wa : 1 - wa) * (b ? wb : 1 - wb) * (c ? wc : 1 - wc);
+                                v += w * uc[(((i64)m * nzc + ic + c) * nyc + ib + b) * nxc + ia + a];
+                            }
+                    u0[m * ne + e] = v;
+                }
+            }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
 /* global assembly (Eq. (5) discretised)                     */
 /* ------------------------------------------------------------------ */
 

@@ -93,6 +93,14 @@ _lib.wd_partition_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)
 _lib.wd_nccl_unique_id.argtypes = [C.c_char_p]
 _lib.wd_nccl_comm_init.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
 _lib.wd_gather_level.argtypes = [_vp]
+_lib.wd_build_mesh.argtypes = [_dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                               C.c_double, _dp, C.c_int, C.c_double, _dp, _dp, _dp, _vp]
+_lib.wd_interp_wind.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                C.c_double, C.c_double, _dp, _dp, _dp, _dp, C.c_int, C.c_int,
+                                C.c_int, _dp, _vp]
+_lib.wd_mass_consistency.argtypes = [_vp, _dp, C.POINTER(C.c_double), _vp]
+_lib.wd_downscale_step.argtypes = [_vp, _dp, _dp, C.c_int, C.c_double, _dp, C.POINTER(wd_report),
+                                   _vp]
 
 # every symbol include/wd.h declares
 ABI_SYMBOLS = ["wd_default_options", "wd_assemble", "wd_rhs", "wd_vcycle", "wd_solve",
@@ -101,7 +109,8 @@ ABI_SYMBOLS = ["wd_default_options", "wd_assemble", "wd_rhs", "wd_vcycle", "wd_s
                "wd_apply", "wd_smooth", "wd_restrict", "wd_prolong", "wd_coarse_solve",
                "wd_residual_norm", "wd_profile_read", "wd_profile_reset", "wd_launch_count",
                "wd_bench_kernel", "wd_partition_rows", "wd_nccl_unique_id", "wd_nccl_comm_init",
-               "wd_gather_level"]
+               "wd_gather_level", "wd_build_mesh", "wd_interp_wind", "wd_mass_consistency",
+               "wd_downscale_step"]
 
 BENCH_KERNELS = {"gs_sweep": 0, "apply": 1, "restrict": 2, "prolong": 3, "vcycle": 4,
                  "residual_norm": 5, "galerkin": 6, "assemble": 7, "gs_sweep_phased": 8}
@@ -360,3 +369,57 @@ def downscale(X, Y, Z, u0, a, rel_tol=1e-8, lam0=None, opt=None):
     finally:
         ctx.close()
     return u, lam, rep
+
+
+# ------------------------------------------------------------------ f4: either side of the path
+def _host_f64(a):
+    import numpy as np
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def wd_build_mesh(zs: torch.Tensor, x0, y0, dx, dy, zeta, H):
+    """Terrain-following mesh (wd.h wd_build_mesh): zs (n2, n1) tensor on the
+    device or host; zeta: the n3 level heights (host sequence); returns X, Y, Z
+    of shape (n3, n2, n1) on zs's device."""
+    z = _host_f64(zeta)
+    n2, n1 = zs.shape
+    n3 = z.size
+    X, Y, Z = (torch.empty((n3, n2, n1), dtype=torch.float64, device=zs.device) for _ in range(3))
+    _check(_lib.wd_build_mesh(_ptr(zs), n1, n2, float(x0), float(y0), float(dx), float(dy),
+                              z.ctypes.data_as(C.c_void_p), n3, float(H), _ptr(X), _ptr(Y),
+                              _ptr(Z), _stream(zs)))
+    return X, Y, Z
+
+
+def wd_interp_wind(uc: torch.Tensor, xc0, yc0, DXc, DYc, hc, X, Y, Z):
+    """Coarse wind uc (3, nzc, nyc, nxc) at heights above ground hc (host
+    sequence) to the element centres of the mesh X, Y, Z (wd_interp_wind)."""
+    h = _host_f64(hc)
+    _, nzc, nyc, nxc = uc.shape
+    n3, n2, n1 = X.shape
+    u0 = torch.empty((3, n3 - 1, n2 - 1, n1 - 1), dtype=torch.float64, device=X.device)
+    _check(_lib.wd_interp_wind(_ptr(uc), nxc, nyc, nzc, float(xc0), float(yc0), float(DXc),
+                               float(DYc), h.ctypes.data_as(C.c_void_p), _ptr(X), _ptr(Y), _ptr(Z),
+                               n1, n2, n3, _ptr(u0), _stream(X)))
+    return u0
+
+
+def wd_mass_consistency(ctx: Context, u):
+    """(l2, max) of the one-point weak divergence D1(u) over free nodes."""
+    out = (C.c_double * 2)()
+    _check(_lib.wd_mass_consistency(ctx.h, _ptr(u), out, _stream(u)))
+    return float(out[0]), float(out[1])
+
+
+def wd_downscale_step(ctx: Context, u0, lam, warm=True, rel_tol=1e-8, u=None,
+                      raise_on_noconv=True):
+    """RHS + (warm-started) solve + wind recovery in one call; lam is updated
+    in place.  Returns (u, report)."""
+    if u is None:
+        u = torch.empty_like(u0)
+    rep = wd_report()
+    rc = _lib.wd_downscale_step(ctx.h, _ptr(u0), _ptr(lam), 1 if warm else 0, float(rel_tol),
+                                _ptr(u), C.byref(rep), _stream(u0))
+    ok = (WD_OK,) if raise_on_noconv else (WD_OK, WD_E_NOCONV, WD_E_DIVERGED, WD_E_NONFINITE)
+    _check(rc, ok)
+    return u, rep.to_dict()

@@ -1287,6 +1287,131 @@ int wd_recover_wind(wd_ctx* ctx, const double* lambda, const double* u0, double*
     return stage_finish(st, {&sl, &su0, &su});
 }
 
+// ------------------------------------------------------------------ f4: either side of the path
+int wd_build_mesh(const double* zs, int n1, int n2, double x0, double y0, double dx, double dy,
+                  const double* zeta, int n3, double H, double* X, double* Y, double* Z,
+                  void* stream) {
+    if (!zs || !zeta || !X || !Y || !Z) return fail(WD_E_INVAL, "NULL argument");
+    if (n1 < 2 || n2 < 2 || n3 < 2) return fail(WD_E_INVAL, "need n1, n2, n3 >= 2");
+    if (!(dx > 0 && dy > 0) || !std::isfinite(dx) || !std::isfinite(dy) || !std::isfinite(x0) ||
+        !std::isfinite(y0) || !std::isfinite(H))
+        return fail(WD_E_INVAL, "dx, dy must be positive and finite; x0, y0, H finite");
+    if (zeta[0] != 0.0) return fail(WD_E_INVAL, "zeta[0] must be 0");
+    for (int k = 1; k < n3; k++)
+        if (!(zeta[k] > zeta[k - 1]) || !std::isfinite(zeta[k]))
+            return fail(WD_E_INVAL, "zeta must be finite and strictly increasing (k = %d)", k);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t N = (size_t)n1 * n2 * n3;
+    Stage sz, sx, sy, szz;
+    RC(stage_in(nullptr, sz, zs, (size_t)n1 * n2, st));
+    RC(stage_out(nullptr, sx, X, N));
+    RC(stage_out(nullptr, sy, Y, N));
+    RC(stage_out(nullptr, szz, Z, N));
+    double* dzeta = nullptr;
+    RC(dalloc(nullptr, (void**)&dzeta, sizeof(double) * n3 + sizeof(unsigned long long)));
+    unsigned long long* dbad = (unsigned long long*)(dzeta + n3);
+    CK(cudaMemcpyAsync(dzeta, zeta, sizeof(double) * n3, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(dbad, 0xff, sizeof(unsigned long long), st));
+    launch_build_mesh(sz.d, n1, n2, n3, x0, y0, dx, dy, dzeta, H, sx.d, sy.d, szz.d, dbad, st);
+    CKL();
+    unsigned long long bad = ~0ull;
+    CK(cudaMemcpyAsync(&bad, dbad, sizeof bad, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    dfree(dzeta);
+    const int rc = stage_finish(st, {&sz, &sx, &sy, &szz});
+    if (rc) return rc;
+    if (bad != ~0ull)
+        return fail(WD_E_MESH, "domain top H = %g is not above the terrain at column (i=%llu, j=%llu)",
+                    H, bad % (unsigned long long)n1, bad / (unsigned long long)n1);
+    return WD_OK;
+}
+
+int wd_interp_wind(const double* uc, int nxc, int nyc, int nzc, double xc0, double yc0,
+                   double DXc, double DYc, const double* hc, const double* X, const double* Y,
+                   const double* Z, int n1, int n2, int n3, double* u0, void* stream) {
+    if (!uc || !hc || !X || !Y || !Z || !u0) return fail(WD_E_INVAL, "NULL argument");
+    if (nxc < 2 || nyc < 2 || nzc < 2) return fail(WD_E_INVAL, "coarse grid needs >= 2 points per direction");
+    if (n1 < 2 || n2 < 2 || n3 < 2) return fail(WD_E_INVAL, "need n1, n2, n3 >= 2");
+    if (!(DXc > 0 && DYc > 0)) return fail(WD_E_INVAL, "coarse spacings must be positive");
+    for (int k = 1; k < nzc; k++)
+        if (!(hc[k] > hc[k - 1])) return fail(WD_E_INVAL, "hc must be strictly increasing (k = %d)", k);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t N = (size_t)n1 * n2 * n3, E = (size_t)3 * (n1 - 1) * (n2 - 1) * (n3 - 1);
+    Stage su, sx, sy, sz, so;
+    RC(stage_in(nullptr, su, uc, (size_t)3 * nxc * nyc * nzc, st));
+    RC(stage_in(nullptr, sx, X, N, st));
+    RC(stage_in(nullptr, sy, Y, N, st));
+    RC(stage_in(nullptr, sz, Z, N, st));
+    RC(stage_out(nullptr, so, u0, E));
+    double* dhc = nullptr;
+    RC(dalloc(nullptr, (void**)&dhc, sizeof(double) * nzc));
+    CK(cudaMemcpyAsync(dhc, hc, sizeof(double) * nzc, cudaMemcpyHostToDevice, st));
+    launch_interp_wind(su.d, nxc, nyc, nzc, xc0, yc0, DXc, DYc, dhc, sx.d, sy.d, sz.d, n1, n2, n3,
+                       so.d, st);
+    CKL();
+    CK(cudaStreamSynchronize(st));   // dhc is freed below
+    dfree(dhc);
+    return stage_finish(st, {&su, &sx, &sy, &sz, &so});
+}
+
+int wd_mass_consistency(wd_ctx* ctx, const double* u, double out[2], void* stream) {
+    if (!ctx || !u || !out) return fail(WD_E_INVAL, "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    Stage su;
+    RC(stage_in(ctx, su, u, abi_elems(ctx), st));
+    const int nb = 1184;
+    const int np = (int)ctx->parts.size();
+    double* per = ctx->dscal + 3000;   // 2 per part
+    for (int p = 0; p < np; p++) {
+        Part& P = ctx->parts[p];
+        Level& F = P.lev[0];
+        // D1(u) = -(RHS kernel applied to u) (reading C12), natural layout in the r buffer
+        Nat d;
+        d.p = F.r;
+        d.n2a = F.L.n2;
+        d.jofs = 0;
+        launch_rhs(P.X, P.Y, P.Z, F.L, nat_elems(ctx, P, su.d), d, st);
+        launch_free_norms(F.L, F.r, P.partial, nb, per + 2 * p, st);
+    }
+    CKL();
+    std::vector<double> h;
+    if (ctx->mode == MODE_NCCL) {
+        double* all = ctx->dscal + 3200;
+        NK(nccl().AllGather(per, all, 2, ncclDouble, ctx->comm, st));
+        h.resize(2 * ctx->nranks);
+        CK(cudaMemcpyAsync(h.data(), all, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+    } else {
+        h.resize(2 * np);
+        CK(cudaMemcpyAsync(h.data(), per, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    double s2 = 0.0, mx = 0.0;
+    for (size_t r = 0; r < h.size() / 2; r++) {   // rank order
+        s2 += h[2 * r];
+        mx = std::max(mx, h[2 * r + 1]);
+    }
+    out[0] = std::sqrt(s2);
+    out[1] = mx;
+    return stage_finish(st, {&su});
+}
+
+int wd_downscale_step(wd_ctx* ctx, const double* u0, double* lambda, int warm, double rel_tol,
+                      double* u, wd_report* rep, void* stream) {
+    if (!ctx || !u0 || !lambda || !u) return fail(WD_E_INVAL, "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    Stage sf;
+    sf.ctx = ctx;
+    sf.bytes = sizeof(double) * abi_nodes(ctx);
+    sf.staged = true;   // a pooled device scratch for f (released by stage_finish)
+    RC(stage_acquire(ctx, sf, sf.bytes));
+    int rc = wd_rhs(ctx, u0, sf.d, stream);
+    int rs = rc ? rc : wd_solve(ctx, sf.d, warm ? lambda : nullptr, rel_tol, lambda, rep, stream);
+    if (rs == WD_OK || rs == WD_E_NOCONV) rc = wd_recover_wind(ctx, lambda, u0, u, stream);
+    const int rf = stage_finish(st, {&sf});
+    if (rs) return rs;
+    return rc ? rc : rf;
+}
+
 int wd_vcycle(wd_ctx* ctx, double* lambda, const double* f, double* rel_res_out, void* stream) {
     if (!ctx || !lambda || !f) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;

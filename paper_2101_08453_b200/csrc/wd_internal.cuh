@@ -141,6 +141,17 @@ void launch_argmin_bottom(const double* Z, int n, double* pval, long long* pidx,
 void launch_gs_fused(const LevDev& L, const double* coef, const double* lin, double* lout,
                      const double* f, cudaStream_t st);
 
+// k_io.cu: steps either side of the path
+void launch_build_mesh(const double* zs, int n1, int n2, int n3, double x0, double y0, double dx,
+                       double dy, const double* zeta, double H, double* X, double* Y, double* Z,
+                       unsigned long long* bad, cudaStream_t st);
+void launch_interp_wind(const double* uc, int nxc, int nyc, int nzc, double xc0, double yc0,
+                        double DXc, double DYc, const double* hc, const double* X,
+                        const double* Y, const double* Z, int n1, int n2, int n3, double* u0,
+                        cudaStream_t st);
+void launch_free_norms(const LevDev& L, const double* v, double* partial, int nb, double* out,
+                       cudaStream_t st);
+
 // k_apply_tma.cu: TMA-staged residual / apply
 int make_coef_maps(const LevDev& L, const double* coef, void* mapA, void* mapB);
 int make_vec_map(const LevDev& L, const double* v, void* map, bool halo);
