@@ -422,6 +422,42 @@ def run_ours(args, ws, rank, local):
                 "cold_start_cycles": rep0["cycles"],
                 "ms_per_step": w0.elapsed_time(w1) / args.warm,
                 "step": "wd_rhs + wd_solve(lambda_{s-1}) + wd_recover_wind (hierarchy reused)"}
+        # SURVEY 8(f) f4 steps around the solve, on the same grid (CUDA events, 3 reps)
+        zs = prob.Z[0].contiguous()
+        jj, ii = divmod(int(torch.argmax(zs)), zs.shape[1])
+        zeta = (prob.Z[:, jj, ii] - zs[jj, ii]).cpu().numpy()
+        zeta[0] = 0.0
+        Htop = float(prob.Z[-1].max())
+        dxm = float(prob.X[0, 0, 1] - prob.X[0, 0, 0])
+        dym = float(prob.Y[0, 1, 0] - prob.Y[0, 0, 0])
+        Lx, Ly = float(prob.X.max()), float(prob.Y.max())
+        nxc, nyc = int(Lx // 1000) + 2, int(Ly // 1000) + 2   # a 1 km "WRF" grid, 12 levels
+        hcs = np.concatenate([[5.0], 5.0 * 1.6 ** np.arange(1, 12)])
+        uc = torch.randn((3, hcs.size, nyc, nxc), dtype=torch.float64, device=dev,
+                         generator=torch.Generator(device=dev).manual_seed(7))
+
+        def evt(fn, reps=3):
+            fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                out = fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / reps, out
+
+        t_mesh, _ = evt(lambda: wd.wd_build_mesh(zs, 0.0, 0.0, dxm, dym, zeta, Htop))
+        t_int, _ = evt(lambda: wd.wd_interp_wind(uc, -500.0, -500.0, 1000.0, 1000.0, hcs,
+                                                 prob.X, prob.Y, prob.Z))
+        t_mc, d_u0 = evt(lambda: wd.wd_mass_consistency(ctx, u0))
+        d_u = wd.wd_mass_consistency(ctx, u)
+        if line is not None:
+            line["pipeline_f4"] = {
+                "build_mesh_ms": t_mesh, "interp_wind_ms": t_int, "mass_consistency_ms": t_mc,
+                "coarse_grid": [nxc, nyc, int(hcs.size)],
+                "D1_l2": {"u0": d_u0[0], "u": d_u[0]},
+                "note": "wd_build_mesh / wd_interp_wind / wd_mass_consistency on the same grid "
+                        "(synchronous entry points: each includes a stream sync)"}
         del ctx, u
     # oracle baseline on the host cores (rank 0, N = 1 only)
     if rank == 0 and ws == 1 and not args.no_cpu:
