@@ -100,18 +100,25 @@ __device__ __forceinline__ int element_stiffness(const double (&x)[8][3], double
                 M[d][e] = det * s;
                 M[e][d] = M[d][e];
             }
+        // v_b = M grad_xi N_b (9 FMA per node), then K_ab += grad_xi N_a . v_b
+        // (3 FMA per pair): 72 + 108 instead of 36 x 9 FMA per Gauss point
 #pragma unroll
-        for (int a = 0; a < 8; a++)
+        for (int b = 0; b < 8; b++) {
+            double v[3];
 #pragma unroll
-            for (int b = a; b < 8; b++) {
+            for (int d = 0; d < 3; d++) {
+                double t = M[d][0] * dN(b, 0, x0, x1, x2);
+                t = fma(M[d][1], dN(b, 1, x0, x1, x2), t);
+                v[d] = fma(M[d][2], dN(b, 2, x0, x1, x2), t);
+            }
+#pragma unroll
+            for (int a = 0; a <= b; a++) {
                 double s = K[ut(a, b)];
 #pragma unroll
-                for (int d = 0; d < 3; d++)
-#pragma unroll
-                    for (int e = 0; e < 3; e++)
-                        s = fma(dN(a, d, x0, x1, x2) * dN(b, e, x0, x1, x2), M[d][e], s);
+                for (int d = 0; d < 3; d++) s = fma(dN(a, d, x0, x1, x2), v[d], s);
                 K[ut(a, b)] = s;
             }
+        }
     }
     return badg;
 }
