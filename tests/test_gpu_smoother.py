@@ -36,6 +36,11 @@ GRIDS = {
                                    dz0=5.0, r=1.1, a=(1, 2, 3)),
     "thin": lambda: synth.hill(nx=3, ny=40, nz=15, dx=30.0, height=50.0, sigma=100.0,
                                dz0=5.0, r=1.15, a=(1, 1, 1)),
+    # degenerate extents: one free column in x, one free plane in z
+    "one_col": lambda: synth.hill(nx=2, ny=70, nz=6, dx=30.0, height=40.0, sigma=200.0,
+                                  dz0=5.0, r=1.2, a=(1, 1, 2)),
+    "one_plane": lambda: synth.hill(nx=90, ny=33, nz=1, dx=30.0, height=40.0, sigma=200.0,
+                                    dz0=5.0, r=1.2, a=(1, 1, 2)),
 }
 
 
