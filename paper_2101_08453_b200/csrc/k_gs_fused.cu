@@ -140,22 +140,50 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
         wrt = act && di >= 0 && di < TI && dj < TJ && j >= L.own0 && j < L.own1;
         own = act ? loff(L, i, j, 0) : 0;
     };
-    // lambda load stream: virtual plane gl = (kl, zl) of tile origin (lI0, lJ0)
-    int kl = 0, zl = 0, lI0 = 0, lJ0 = 0;
-    if (G > 0) origin(0, lI0, lJ0);
+    // lambda load stream: virtual plane gl = (kl, zl).  Each thread fills the
+    // ring entries e = threadIdx.x + q THREADS (q < NE) of every plane; their
+    // offsets relative to the tile origin are fixed, so per plane only the
+    // tile base and the plane stride change.
+    constexpr int NE = (PL + THREADS - 1) / THREADS;
+    i64 eoff[NE];
+    int eri[NE], erj[NE];
+#pragma unroll
+    for (int q = 0; q < NE; q++) {
+        const int e = (int)threadIdx.x + q * THREADS;
+        const int rj = e / RW, r = e - rj * RW;
+        const int half = r >= SW, pos = r - half * SW;
+        erj[q] = e < PL ? rj : -1000000;   // never valid beyond the ring
+        eri[q] = 2 * pos + half;
+        // loff(i, j, 0) - loff(I0 - 4, J0 - 1, 0) for i = I0 - 4 + ri (I0 even), j = J0 - 1 + rj
+        eoff[q] = (i64)rj * L.sj + (i64)half * L.H + pos;
+    }
+    int kl = 0, zl = 0;
+    i64 lbase = 0;        // loff(I0 - 4 (even part), J0 - 1, zl) of the loading tile
+    unsigned lvalid = 0;  // bit q: entry q lies inside the grid
+    auto load_tile = [&](int k) {
+        int I0, J0;
+        origin(k, I0, J0);
+        lbase = (i64)(J0 - 1) * L.sj + (I0 >> 1) - 2;
+        lvalid = 0;
+#pragma unroll
+        for (int q = 0; q < NE; q++) {
+            const int i = I0 - 4 + eri[q], j = J0 - 1 + erj[q];
+            if (eri[q] >= 1 && i >= 0 && i < L.n1 && j >= 0 && j < L.n2) lvalid |= 1u << q;
+        }
+    };
+    if (G > 0) load_tile(0);
     auto load_next = [&]() {
         double* dst = ring + ((kl * n3 + zl) & (RING - 1)) * PL;
-        for (int t = threadIdx.x; t < PL; t += THREADS) {
-            const int rj = t / RW, r = t - rj * RW;
-            const int half = r >= SW, pos = r - half * SW;
-            const int ri = 2 * pos + half;
-            const int i = lI0 - 4 + ri, j = lJ0 - 1 + rj;
-            if (ri >= 1 && i >= 0 && i < L.n1 && j >= 0 && j < L.n2) cp_async8(dst + t, lin + loff(L, i, j, zl));
-            else dst[t] = 0.0;
+        const i64 pb = lbase + (i64)zl * L.sk;
+#pragma unroll
+        for (int q = 0; q < NE; q++) {
+            const int e = (int)threadIdx.x + q * THREADS;
+            if (lvalid & (1u << q)) cp_async8(dst + e, lin + pb + eoff[q]);
+            else if (e < PL) dst[e] = 0.0;
         }
         if (++zl == n3) {
             zl = 0;
-            if (++kl < ntk) origin(kl, lI0, lJ0);
+            if (++kl < ntk) load_tile(kl);
         }
     };
     __syncthreads();   // ring zeroed before the first copies land
