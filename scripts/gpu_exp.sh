@@ -1,7 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-for e in 1 0 1; do
-  echo "stage=$e" >> gpurun_out/exp.log
-  WD_GS_STAGE=$e timeout 300 python -m pytest tests/test_gpu_smoother.py tests/test_gpu_dist.py -x -q 2>&1 | tail -1 >> gpurun_out/exp.log
-  WD_GS_STAGE=$e timeout 300 python scripts/kbench.py --only gs_sweep,vcycle >> gpurun_out/exp.log 2>&1
-done
+timeout 300 python -m pytest tests/test_gpu_smoother.py -x -q -k every_level 2>&1 | tail -1 >> gpurun_out/exp.log
+timeout 300 python scripts/kbench.py --only gs_sweep,vcycle >> gpurun_out/exp.log 2>&1
