@@ -153,3 +153,42 @@ def test_fullsize_solution_residual(big, wd):
     # exact zeros on the Dirichlet set
     assert not lam[-1].any() and not lam[:, 0].any() and not lam[:, -1].any()
     assert not lam[:, :, 0].any() and not lam[:, :, -1].any()
+
+
+def test_fullsize_sweep_gs_equations(big, wd):
+    """One fused smoother sweep at full size, checked against the
+    oracle's element matrices at sampled nodes of the LAST colour (i, j odd):
+    when they are updated every neighbour is final except the one above in the
+    same column (bottom-up: still the input value), so
+    K_pp x_p = f_p - sum_{q != p} K_pq x_q  with x_q the output, and the input
+    for q = p + (0,0,1), holds to rounding; and the fused sweep equals the four
+    colour-phase launches bit for bit."""
+    ctx, p = big["ctx"], big["p"]
+    X, Y, Z = big["XYZ"]
+    n1, n2, n3 = p.dims
+    g = torch.Generator(device=DEV).manual_seed(5)
+    x0 = torch.rand((n3, n2, n1), dtype=torch.float64, device=DEV, generator=g) * 2 - 1
+    f = big["f"]
+    x1 = wd.wd_smooth(ctx, 0, x0.clone(), f, sweeps=1)
+    rng = np.random.default_rng(23)
+    pts = np.stack([2 * rng.integers(0, (n1 - 2) // 2, 60) + 1, 2 * rng.integers(0, (n2 - 2) // 2, 60) + 1,
+                    rng.integers(0, n3 - 1, 60)], 1)
+    for (i, j, k) in pts:
+        row = _node_row27(X, Y, Z, p.a, i, j, k)
+        nb = np.zeros(27)
+        for o in range(27):
+            dx, dy, dz = o % 3 - 1, (o // 3) % 3 - 1, o // 9 - 1
+            kk = k + dz
+            if 0 <= kk < n3:
+                nb[o] = float(x1[kk, j + dy, i + dx])
+        # the node above: its input value (0 on the Dirichlet top plane)
+        nb[22] = float(x0[k + 1, j, i]) if k + 1 < n3 - 1 else 0.0
+        r = float(f[k, j, i]) - row @ nb
+        assert abs(r) <= 1e-12 * (float(np.abs(row * nb).sum()) + abs(float(f[k, j, i]))), (i, j, k)
+    # the same sweep as four colour-phase launches (a second context, phased)
+    opt = wd.default_options(smoother="phased")
+    cph = wd.wd_assemble(p.X, p.Y, p.Z, p.a, opt)
+    x2 = wd.wd_smooth(cph, 0, x0.clone(), f, sweeps=1)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x2)
+    cph.close()
