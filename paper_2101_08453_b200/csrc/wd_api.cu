@@ -201,6 +201,9 @@ struct wd_ctx {
     double* dscal = nullptr;   // device scalars
     double* hscal = nullptr;   // pinned host scalars
     cudaStream_t cap = nullptr;
+    // host-pointer pipelining (copy-in / compute + copy-out streams, chunk events)
+    cudaStream_t pin_s = nullptr, pout_s = nullptr;
+    cudaEvent_t pev[17] = {};
     cudaGraphExec_t vgraph = nullptr;
     long long bytes = 0;
     std::vector<std::pair<void*, size_t>> pool;   // staging buffers for host pointers
@@ -826,6 +829,9 @@ void wd_destroy(wd_ctx* ctx) {
     cudaGetLastError();
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
     if (ctx->cap) cudaStreamDestroy(ctx->cap);
+    if (ctx->pin_s) cudaStreamDestroy(ctx->pin_s);
+    if (ctx->pout_s) cudaStreamDestroy(ctx->pout_s);
+    for (auto e : ctx->pev) if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_gs) if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_cyc) if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_res) if (e) cudaEventDestroy(e);
@@ -1273,9 +1279,75 @@ int wd_rhs(wd_ctx* ctx, const double* u0, double* f, void* stream) {
     return stage_finish(st, {&su, &sf});
 }
 
+// Host-pointer recovery on one GPU, pipelined over chunks of element rows:
+// the copy-in of chunk c+1 (lambda node rows, u0 element rows) runs on one
+// stream while chunk c is recovered and copied out on another, so the PCIe
+// directions overlap (H2D and D2H use separate copy engines).
+static int recover_pipelined(wd_ctx* ctx, const double* lambda, const double* u0, double* u,
+                             cudaStream_t st) {
+    constexpr int NCH = 8;
+    if (!ctx->pin_s) {
+        CK(cudaStreamCreateWithFlags(&ctx->pin_s, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->pout_s, cudaStreamNonBlocking));
+        for (auto& e : ctx->pev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    Part& P = ctx->parts[0];
+    const LevDev& L0 = P.lev[0].L;
+    const int n1 = ctx->n1, n2 = ctx->n2, n3 = ctx->n3, nx = n1 - 1, ny = n2 - 1, nz = n3 - 1;
+    const bool hl = !is_device_ptr(lambda), hu0 = !is_device_ptr(u0), hu = !is_device_ptr(u);
+    Stage sl, su0, su;
+    sl.ctx = su0.ctx = su.ctx = ctx;
+    double *dl = const_cast<double*>(lambda), *du0 = const_cast<double*>(u0), *du = u;
+    if (hl) { sl.staged = true; RC(stage_acquire(ctx, sl, sizeof(double) * abi_nodes(ctx))); dl = sl.d; }
+    if (hu0) { su0.staged = true; RC(stage_acquire(ctx, su0, sizeof(double) * abi_elems(ctx))); du0 = su0.d; }
+    if (hu) { su.staged = true; RC(stage_acquire(ctx, su, sizeof(double) * abi_elems(ctx))); du = su.d; }
+    cudaEvent_t* ev = ctx->pev;
+    CK(cudaEventRecord(ev[16], st));   // after the caller's prior work
+    CK(cudaStreamWaitEvent(ctx->pin_s, ev[16], 0));
+    CK(cudaStreamWaitEvent(ctx->pout_s, ev[16], 0));
+    const size_t nplane = (size_t)n1 * n2, eplane = (size_t)nx * ny;
+    for (int c = 0; c < NCH; c++) {
+        const int r0 = (int)((long long)ny * c / NCH), r1 = (int)((long long)ny * (c + 1) / NCH);
+        if (r1 <= r0) continue;
+        if (hl) {   // node rows r0 .. r1 (inclusive) of every plane
+            const size_t off = (size_t)r0 * n1, w = (size_t)(r1 + 1 - r0) * n1;
+            CK(cudaMemcpy2DAsync(dl + off, sizeof(double) * nplane, lambda + off, sizeof(double) * nplane,
+                                 sizeof(double) * w, n3, cudaMemcpyHostToDevice, ctx->pin_s));
+        }
+        if (hu0) {  // element rows r0 .. r1-1 of every (component, plane)
+            const size_t off = (size_t)r0 * nx, w = (size_t)(r1 - r0) * nx;
+            CK(cudaMemcpy2DAsync(du0 + off, sizeof(double) * eplane, u0 + off, sizeof(double) * eplane,
+                                 sizeof(double) * w, (size_t)3 * nz, cudaMemcpyHostToDevice, ctx->pin_s));
+        }
+        CK(cudaEventRecord(ev[c], ctx->pin_s));
+        CK(cudaStreamWaitEvent(ctx->pout_s, ev[c], 0));
+        LevDev L = L0;
+        L.own0 = r0;
+        L.own1 = r1;
+        launch_recover(P.X, P.Y, P.Z, L, ctx->c, nat_nodes(ctx, P, dl), nat_elems(ctx, P, du0),
+                       nat_elems(ctx, P, du), ctx->pout_s);
+        if (hu) {
+            const size_t off = (size_t)r0 * nx, w = (size_t)(r1 - r0) * nx;
+            CK(cudaMemcpy2DAsync(u + off, sizeof(double) * eplane, du + off, sizeof(double) * eplane,
+                                 sizeof(double) * w, (size_t)3 * nz, cudaMemcpyDeviceToHost, ctx->pout_s));
+        }
+    }
+    CKL();
+    CK(cudaEventRecord(ev[8], ctx->pout_s));
+    CK(cudaEventRecord(ev[9], ctx->pin_s));
+    CK(cudaStreamWaitEvent(st, ev[8], 0));
+    CK(cudaStreamWaitEvent(st, ev[9], 0));
+    CK(cudaStreamSynchronize(st));   // host outputs complete on return
+    for (Stage* x : {&sl, &su0, &su})
+        if (x->staged && x->slot >= 0) ctx->pool_busy[x->slot] = 0;
+    return WD_OK;
+}
+
 int wd_recover_wind(wd_ctx* ctx, const double* lambda, const double* u0, double* u, void* stream) {
     if (!ctx || !lambda || !u0 || !u) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
+    if (ctx->mode == MODE_SINGLE && (!is_device_ptr(lambda) || !is_device_ptr(u0) || !is_device_ptr(u)))
+        return recover_pipelined(ctx, lambda, u0, u, st);
     Stage sl, su0, su;
     RC(stage_in(ctx, sl, lambda, abi_nodes(ctx), st));
     RC(stage_in(ctx, su0, u0, abi_elems(ctx), st));

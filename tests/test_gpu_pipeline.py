@@ -128,3 +128,30 @@ def test_downscale_step_equals_its_parts_and_warm_restart(wd):
     assert rep3["cycles"] <= 1
     assert torch.allclose(u3, u, rtol=0, atol=1e-8 * float(u.abs().max()))
     ctx.close()
+
+
+def test_recover_host_pointer_pipeline(wd):
+    """wd_recover_wind with host arrays runs chunk-pipelined (copy-in of one
+    chunk of element rows overlapping the recovery and copy-out of the
+    previous one); every mix of host / device arguments gives the device
+    result bit for bit (ragged row count: uneven chunks)."""
+    import itertools
+    p = synth.hill(nx=61, ny=77, nz=7, dx=40.0, height=150.0, sigma=400.0, dz0=8.0, r=1.2,
+                   a=(1, 1, 5), device=DEV)
+    ctx = wd.wd_assemble(p.X, p.Y, p.Z, p.a, wd.default_options(coarsest_max_free=100))
+    f = wd.wd_rhs(ctx, p.u0)
+    lam, _ = wd.wd_solve(ctx, f, rel_tol=1e-9)
+    ref = wd.wd_recover_wind(ctx, lam, p.u0)
+    torch.cuda.synchronize()
+    for hl, hu0, hu in itertools.product([False, True], repeat=3):
+        if not (hl or hu0 or hu):
+            continue
+        l_ = lam.cpu().pin_memory() if hl else lam
+        u0_ = p.u0.cpu().pin_memory() if hu0 else p.u0
+        out = torch.empty(p.u0.shape, dtype=torch.float64, device="cpu" if hu else DEV)
+        if hu:
+            out = out.pin_memory()
+        got = wd.wd_recover_wind(ctx, l_, u0_, out)
+        torch.cuda.synchronize()
+        assert torch.equal(got.cpu(), ref.cpu()), (hl, hu0, hu)
+    ctx.close()
