@@ -161,11 +161,12 @@ __device__ __forceinline__ void gather_couplings(const double* ke, int t, double
 __global__ void __launch_bounds__(NTH, 1)
 assemble_kernel(const double* __restrict__ X, const double* __restrict__ Y,
                 const double* __restrict__ Z, int n1, int n2, int n3, double c0, double c1,
-                double c2, LevDev L, double* __restrict__ coef, unsigned long long* bad) {
+                double c2, LevDev L, double* __restrict__ coef, unsigned long long* bad,
+                int ty0) {
     extern __shared__ double ke[];   // [36][NTH]
     const int t = threadIdx.x;
     const int tx = t % TX, ty = t / TX;
-    const int i0 = blockIdx.x * (TX - 1), j0 = blockIdx.y * (TY - 1);
+    const int i0 = blockIdx.x * (TX - 1), j0 = (blockIdx.y + ty0) * (TY - 1);
     const int ei = i0 - 1 + tx, ej = j0 - 1 + ty;
     const bool ev = ei >= 0 && ei < n1 - 1 && ej >= 0 && ej < n2 - 1;
     const int ni = i0 + tx, nj = j0 + ty;
@@ -348,13 +349,19 @@ recover_kernel(const double* __restrict__ X, const double* __restrict__ Y,
 
 void launch_assemble(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
                      const double c[3], const LevDev& L, double* coef, unsigned long long* bad,
-                     cudaStream_t st) {
+                     cudaStream_t st, int ty0, int ty1) {
     const size_t smem = sizeof(double) * 36 * NTH;
     cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid((n1 + TX - 2) / (TX - 1), (n2 + TY - 2) / (TY - 1));
+    const int nty = (n2 + TY - 2) / (TY - 1);
+    if (ty1 < 0 || ty1 > nty) ty1 = nty;
+    if (ty1 <= ty0) return;
+    dim3 grid((n1 + TX - 2) / (TX - 1), ty1 - ty0);
     g_launches += 1;
-    assemble_kernel<<<grid, NTH, smem, st>>>(X, Y, Z, n1, n2, n3, c[0], c[1], c[2], L, coef, bad);
+    assemble_kernel<<<grid, NTH, smem, st>>>(X, Y, Z, n1, n2, n3, c[0], c[1], c[2], L, coef, bad, ty0);
 }
+
+int assemble_tile_rows(int n2) { return (n2 + TY - 2) / (TY - 1); }
+int assemble_rows_needed(int t) { return t * (TY - 1) + TY; }   // node rows [0, .) tile row t reads
 
 void launch_rhs(const double* X, const double* Y, const double* Z, const LevDev& L, Nat u0, Nat f,
                 cudaStream_t st) {

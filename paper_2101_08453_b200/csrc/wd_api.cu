@@ -881,6 +881,8 @@ void wd_partition_rows(int n2, int nranks, int rank, int* j_begin, int* j_end) {
     *j_end = (int)((long long)n2 * (rank + 1) / nranks);
 }
 
+int ensure_pipe(wd_ctx* ctx);
+
 static int assemble_impl(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
                          double a1, double a2, double a3, const wd_options* opt, cudaStream_t st,
                          wd_ctx* ctx) {
@@ -926,8 +928,34 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
         P.jhi = ctx->nranks > 1 ? std::min(P.own1g + HALO, n2) : n2;
     }
 
-    // ---- coordinates: internal copies of the part's rows (natural layout)
-    {
+    // ---- coordinates: internal copies of the part's rows (natural layout).
+    // Host arrays on one GPU: copied straight into the internal copies in
+    // chunks of node rows on a copy stream; the level-0 assembly below starts
+    // on each chunk's tile rows as soon as their rows have arrived.
+    const bool piped = ctx->mode == MODE_SINGLE && !is_device_ptr(X) && !is_device_ptr(Y) &&
+                       !is_device_ptr(Z);
+    constexpr int NCH = 8;
+    int chunk_rows[NCH + 1] = {0};
+    if (piped) {
+        RC(ensure_pipe(ctx));
+        Part& P = ctx->parts[0];
+        const size_t n = (size_t)n1 * n2 * n3, plane = (size_t)n1 * n2;
+        double** dst[3] = {&P.X, &P.Y, &P.Z};
+        const double* src[3] = {X, Y, Z};
+        for (int d = 0; d < 3; d++) RC(dalloc(ctx, (void**)dst[d], sizeof(double) * n));
+        CK(cudaEventRecord(ctx->pev[16], st));
+        CK(cudaStreamWaitEvent(ctx->pin_s, ctx->pev[16], 0));
+        for (int c = 0; c < NCH; c++) {
+            const int r0 = (int)((long long)n2 * c / NCH), r1 = (int)((long long)n2 * (c + 1) / NCH);
+            chunk_rows[c + 1] = r1;
+            for (int d = 0; d < 3; d++)
+                CK(cudaMemcpy2DAsync(*dst[d] + (size_t)r0 * n1, sizeof(double) * plane,
+                                     src[d] + (size_t)r0 * n1, sizeof(double) * plane,
+                                     sizeof(double) * (size_t)(r1 - r0) * n1, n3,
+                                     cudaMemcpyHostToDevice, ctx->pin_s));
+            CK(cudaEventRecord(ctx->pev[c], ctx->pin_s));
+        }
+    } else {
         const size_t N = abi_nodes(ctx);
         Stage sx, sy, sz;
         RC(stage_in(nullptr, sx, X, N, st));
@@ -973,7 +1001,25 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
         L0.cown1 = L0.L.own1;
         RC(alloc_level(ctx, L0));
         CK(cudaMemsetAsync(dbad, 0xff, sizeof(unsigned long long), st));
-        launch_assemble(P.X, P.Y, P.Z, n1, rows, n3, ctx->c, L0.L, L0.coef, dbad, st);
+        if (piped) {
+            // tile rows whose node rows have all arrived, chunk by chunk
+            CK(cudaEventRecord(ctx->pev[15], st));
+            CK(cudaStreamWaitEvent(ctx->pout_s, ctx->pev[15], 0));
+            const int nty = assemble_tile_rows(rows);
+            int t0 = 0;
+            for (int c = 0; c < NCH; c++) {
+                int t1 = t0;
+                while (t1 < nty && (assemble_rows_needed(t1) <= chunk_rows[c + 1] || c == NCH - 1)) t1++;
+                CK(cudaStreamWaitEvent(ctx->pout_s, ctx->pev[c], 0));
+                launch_assemble(P.X, P.Y, P.Z, n1, rows, n3, ctx->c, L0.L, L0.coef, dbad, ctx->pout_s,
+                                t0, t1);
+                t0 = t1;
+            }
+            CK(cudaEventRecord(ctx->pev[14], ctx->pout_s));
+            CK(cudaStreamWaitEvent(st, ctx->pev[14], 0));
+        } else {
+            launch_assemble(P.X, P.Y, P.Z, n1, rows, n3, ctx->c, L0.L, L0.coef, dbad, st);
+        }
         CKL();
         unsigned long long hb;
         CK(cudaMemcpyAsync(&hb, dbad, sizeof hb, cudaMemcpyDeviceToHost, st));
@@ -1279,6 +1325,15 @@ int wd_rhs(wd_ctx* ctx, const double* u0, double* f, void* stream) {
     return stage_finish(st, {&su, &sf});
 }
 
+int ensure_pipe(wd_ctx* ctx) {
+    if (!ctx->pin_s) {
+        CK(cudaStreamCreateWithFlags(&ctx->pin_s, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->pout_s, cudaStreamNonBlocking));
+        for (auto& e : ctx->pev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return WD_OK;
+}
+
 // Host-pointer recovery on one GPU, pipelined over chunks of element rows:
 // the copy-in of chunk c+1 (lambda node rows, u0 element rows) runs on one
 // stream while chunk c is recovered and copied out on another, so the PCIe
@@ -1286,11 +1341,7 @@ int wd_rhs(wd_ctx* ctx, const double* u0, double* f, void* stream) {
 static int recover_pipelined(wd_ctx* ctx, const double* lambda, const double* u0, double* u,
                              cudaStream_t st) {
     constexpr int NCH = 8;
-    if (!ctx->pin_s) {
-        CK(cudaStreamCreateWithFlags(&ctx->pin_s, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&ctx->pout_s, cudaStreamNonBlocking));
-        for (auto& e : ctx->pev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
+    RC(ensure_pipe(ctx));
     Part& P = ctx->parts[0];
     const LevDev& L0 = P.lev[0].L;
     const int n1 = ctx->n1, n2 = ctx->n2, n3 = ctx->n3, nx = n1 - 1, ny = n2 - 1, nz = n3 - 1;

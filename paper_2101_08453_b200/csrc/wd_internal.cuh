@@ -91,9 +91,13 @@ __host__ __device__ __forceinline__ int slot_of(int dx, int dy, int dz) {
 // (all stream-ordered on `st`; defined in the .cu files)
 
 // k_fe.cu: finite elements
+// tile rows [ty0, ty1) of the assembly grid (ty1 < 0: all); assemble_rows_needed(t):
+// node rows [0, .) the tile rows < t+1 read (for chunked host copies)
 void launch_assemble(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
                      const double c[3], const LevDev& L, double* coef,
-                     unsigned long long* bad, cudaStream_t st);
+                     unsigned long long* bad, cudaStream_t st, int ty0 = 0, int ty1 = -1);
+int assemble_tile_rows(int n2);
+int assemble_rows_needed(int t);
 void launch_rhs(const double* X, const double* Y, const double* Z, const LevDev& L, Nat u0, Nat f,
                 cudaStream_t st);
 void launch_recover(const double* X, const double* Y, const double* Z, const LevDev& L,

@@ -155,3 +155,20 @@ def test_recover_host_pointer_pipeline(wd):
         torch.cuda.synchronize()
         assert torch.equal(got.cpu(), ref.cpu()), (hl, hu0, hu)
     ctx.close()
+
+
+def test_assemble_from_host_arrays_pipelined(wd):
+    """wd_assemble with host X, Y, Z copies the coordinates in row chunks and
+    starts the assembly of each chunk's tile rows as they arrive: the operator
+    on every level equals the device-input assembly bit for bit."""
+    p = synth.hill(nx=150, ny=93, nz=9, dx=40.0, height=200.0, sigma=600.0, dz0=8.0, r=1.2,
+                   a=(1, 1, 10))
+    g = p.to(DEV)
+    opt = wd.default_options(coarsest_max_free=100)
+    cd = wd.wd_assemble(g.X, g.Y, g.Z, p.a, opt)
+    ch = wd.wd_assemble(p.X.pin_memory(), p.Y.pin_memory(), p.Z.pin_memory(), p.a, opt)
+    assert cd.num_levels() == ch.num_levels()
+    for l in range(cd.num_levels()):
+        assert torch.equal(wd.wd_get_stencil(cd, l).cpu(), wd.wd_get_stencil(ch, l).cpu()), l
+    cd.close()
+    ch.close()
