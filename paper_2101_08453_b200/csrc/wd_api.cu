@@ -29,6 +29,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <ctime>
 #include <vector>
 
 using namespace wd;
@@ -44,6 +45,30 @@ int fail(int code, const char* fmt, ...) {
     va_end(ap);
     return code;
 }
+
+// development: WD_SETUP_TIMING=1 prints the setup phases (stream-synchronised)
+struct PhaseTimer {
+    bool on = false;
+    double t0 = 0;
+    cudaStream_t st = nullptr;
+    static double now() {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+    }
+    void start(cudaStream_t s) {
+        on = getenv("WD_SETUP_TIMING") != nullptr;
+        st = s;
+        if (on) { cudaStreamSynchronize(st); t0 = now(); }
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const double t = now();
+        fprintf(stderr, "[wd setup] %-28s %8.2f ms\n", what, t - t0);
+        t0 = t;
+    }
+};
 
 #define CK(call)                                                                               \
     do {                                                                                       \
@@ -896,6 +921,8 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
     if (opt) ctx->opt = *opt;
     else wd_default_options(&ctx->opt);
     const wd_options& o = ctx->opt;
+    PhaseTimer PT;
+    PT.start(st);
     // ---- decomposition
     ctx->nranks = o.nranks > 1 ? o.nranks : 1;
     if (ctx->nranks == 1) ctx->mode = MODE_SINGLE;
@@ -928,6 +955,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
         P.jhi = ctx->nranks > 1 ? std::min(P.own1g + HALO, n2) : n2;
     }
 
+    PT.mark("decomposition");
     // ---- coordinates: internal copies of the part's rows (natural layout).
     // Host arrays on one GPU: copied straight into the internal copies in
     // chunks of node rows on a copy stream; the level-0 assembly below starts
@@ -987,6 +1015,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
         for (auto& e : ctx->ev_res) CK(cudaEventCreate(&e));
     }
 
+    PT.mark("coordinates + ctx");
     // ---- level 0: assembly fused with validation
     const bool multi = ctx->nranks > 1;
     unsigned long long* dbad = (unsigned long long*)(ctx->dscal + 8);
@@ -1065,6 +1094,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
     }
     RC(exchange(ctx, 0, ARR_COEF, HALO, st));   // rows at the slab edges come from the neighbours
 
+    PT.mark("level-0 assembly");
     // ---- planner inputs (reading C2): h1 = sqrt(dx dy); h3 at the column of minimum Z(i,j,0)
     double h1;
     double h3[MAXNZ], h3n[MAXNZ], h1n;
@@ -1142,6 +1172,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
         for (int k = 0; k + 1 < n3; k++) h3[k] = zc[k + 1] - zc[k];
     }
 
+    PT.mark("planner inputs");
     // ---- hierarchy
     while (ctx->nlev < MAXLEV) {
         const int l = ctx->nlev - 1;
@@ -1252,6 +1283,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
         h1 = h1n;
         for (int t = 0; t + 1 < nk; t++) h3[t] = h3n[t];
     }
+    PT.mark("hierarchy (plan+Galerkin)");
     // ---- coarsest level (reading C8): replicated or single
     {
         const int l = ctx->nlev - 1;
@@ -1272,6 +1304,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
             }
         }
     }
+    PT.mark("coarsest inverse");
     CK(cudaStreamSynchronize(st));
     CKL();
     return WD_OK;
