@@ -77,3 +77,21 @@ def test_virtual_ranks_partition_rules(wd):
     f = wd.wd_rhs(ctx, p.u0)
     lam, rep = wd.wd_solve(ctx, f, rel_tol=1e-10)
     assert rep["converged"]
+
+
+def test_virtual_ranks_f4_entry_points(wd):
+    """Diagnostics and the one-call time step on 3 slabs equal one part:
+    wd_mass_consistency (norms summed in rank order) and wd_downscale_step."""
+    p = PROBLEMS["ragged"]()
+    ref = _ctx(wd, p, 1, 0)
+    ctx = _ctx(wd, p, 3, 1000)
+    a = wd.wd_mass_consistency(ref, p.u0)
+    b = wd.wd_mass_consistency(ctx, p.u0)
+    assert abs(a[0] - b[0]) <= 1e-12 * a[0] and a[1] == b[1]
+    l1 = torch.zeros(ref.node_shape, dtype=torch.float64, device=DEV)
+    lR = l1.clone()
+    u1, r1 = wd.wd_downscale_step(ref, p.u0, l1, warm=False, rel_tol=1e-9)
+    uR, rR = wd.wd_downscale_step(ctx, p.u0, lR, warm=False, rel_tol=1e-9)
+    assert r1["cycles"] == rR["cycles"] and torch.equal(l1, lR) and torch.equal(u1, uR)
+    ctx.close()
+    ref.close()
