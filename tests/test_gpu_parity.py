@@ -258,3 +258,30 @@ def test_rules_hierarchy_and_solve(wd, rule):
     assert rep["cycles"] == ro["cycles"]
     if ro["status"] == 0:
         assert np.linalg.norm(_n(lam) - lo) / np.linalg.norm(lo) <= 1e-8
+
+
+def test_warm_start_sequence_parity(case, wd):
+    """BASELINE configs[4] in miniature: u0 perturbed by a smooth
+    increment, each solve warm-started from the previous lambda, on both
+    sides: lambda <= 1e-8 rel l2 and the same number of cycles (+-1) at every
+    step, initial residuals within 1e-10 relative."""
+    ctx, mg, p = case["ctx"], case["mg"], case["p"]
+    X, Y, Z, u0 = case["np"]
+    rng = np.random.default_rng(31)
+    nz, ny, nx = u0.shape[1:]
+    yy, xx = np.meshgrid(np.linspace(0, 1, ny), np.linspace(0, 1, nx), indexing="ij")
+    lam_g, lam_o = None, None
+    u = u0.copy()
+    for step in range(3):
+        a, b = rng.normal(0, 0.5, 2)
+        u[0] += a * np.sin(np.pi * xx)[None] * np.cos(np.pi * yy)[None]
+        u[1] += b * np.cos(np.pi * xx)[None] * np.sin(np.pi * yy)[None]
+        fo = oracle.rhs(X, Y, Z, u)
+        lo, ro = mg.solve(fo, lam0=lam_o, tol=1e-10, max_cycles=100)
+        fg = wd.wd_rhs(ctx, _t(u))
+        lg, rg = wd.wd_solve(ctx, fg, lam0=lam_g, rel_tol=1e-10)
+        ln = _n(lg)
+        assert np.linalg.norm(ln - lo) <= 1e-8 * np.linalg.norm(lo), step
+        assert abs(rg["cycles"] - ro["cycles"]) <= 1, (step, rg["cycles"], ro["cycles"])
+        assert abs(rg["rel_res0"] - ro["hist"][0]) <= 1e-10 * max(ro["hist"][0], 1e-300), step
+        lam_g, lam_o = lg, lo
