@@ -1,0 +1,6 @@
+# per-launch DRAM bytes + duration of every kernel of one bench step (ncu; serialized, cold)
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+CMD="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --warm 0"
+timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/dram.csv $CMD > gpurun_out/ncu_dram.log 2>&1
+echo "rc=$?" >> gpurun_out/ncu_dram.log
