@@ -1626,9 +1626,15 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
     R.coarse_direct = ctx->coarse_direct;
     R.coarse_free = ctx->nf;
     RC(norm_sq(ctx, ARR_F, 1, st));
-    RC(residual_sq(ctx, 0, st));
-    RC(fetch_scalars(ctx, 2, st));
-    profile_accumulate(ctx, false, true);
+    if (lambda0) {
+        RC(residual_sq(ctx, 0, st));
+        RC(fetch_scalars(ctx, 2, st));
+        profile_accumulate(ctx, false, true);
+    } else {
+        // zero start: f - K 0 = f exactly, no residual pass needed
+        RC(fetch_scalars(ctx, 2, st));
+        ctx->hscal[0] = ctx->hscal[1];
+    }
     const double fn = std::sqrt(ctx->hscal[1]);
     int status = WD_E_NOCONV;
     int c = 0;
