@@ -167,3 +167,24 @@ def test_line_relaxation_solve_parity(wd, name):
     assert np.linalg.norm(lam - lo) <= 1e-8 * np.linalg.norm(lo)
     assert abs(rep["rate"] - ro["rate"]) <= 0.1 * ro["rate"], (rep["rate"], ro["rate"])
     ctx.close()
+
+
+@pytest.mark.parametrize("nx,ny", [(64, 8), (65, 9), (66, 10), (127, 15), (128, 16), (129, 17),
+                                   (63, 7), (62, 23)])
+def test_fused_tile_edges(wd, nx, ny):
+    """Grids whose node counts sit on, just below and just above the fused
+    sweep's 64 x 8 tile boundaries: fused == phased bit for bit on the fine
+    level (two sweeps, ping-pong both ways)."""
+    p = synth.hill(nx=nx, ny=ny, nz=5, dx=30.0, height=60.0, sigma=300.0, dz0=6.0, r=1.2,
+                   a=(1, 1, 4))
+    g, (cf, cp) = _pair(wd, p)
+    rng = np.random.default_rng(nx * 100 + ny)
+    n1, n2, n3 = cf.level_dims(0)
+    x = torch.as_tensor(rng.uniform(-1, 1, (n3, n2, n1)), device=DEV)
+    f = torch.as_tensor(rng.uniform(-1, 1, (n3, n2, n1)), device=DEV)
+    a = wd.wd_smooth(cf, 0, x.clone(), f, sweeps=2)
+    b = wd.wd_smooth(cp, 0, x.clone(), f, sweeps=2)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    cf.close()
+    cp.close()
