@@ -172,3 +172,22 @@ def test_assemble_from_host_arrays_pipelined(wd):
         assert torch.equal(wd.wd_get_stencil(cd, l).cpu(), wd.wd_get_stencil(ch, l).cpu()), l
     cd.close()
     ch.close()
+
+
+def test_example_downscale_demo_runs():
+    """examples/downscale_demo.py (mesh -> interpolation -> hierarchy -> warm
+    time steps -> diagnostics) at a small size."""
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "examples", "downscale_demo.py"),
+                          "--nx", "64", "--ny", "48", "--nz", "8", "--steps", "3"],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    rows = [l.split() for l in out.stdout.splitlines() if l.strip() and l.split()[0].isdigit()]
+    assert len(rows) == 3
+    for r in rows:
+        assert float(r[3]) <= 1e-8            # converged
+        assert float(r[5]) < float(r[4])      # projected wind more mass-consistent than u0
+    assert int(rows[1][1]) < int(rows[0][1])  # warm start needs fewer cycles
