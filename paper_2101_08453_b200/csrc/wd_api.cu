@@ -1555,15 +1555,22 @@ int wd_downscale_step(wd_ctx* ctx, const double* u0, double* lambda, int warm, d
                       double* u, wd_report* rep, void* stream) {
     if (!ctx || !u0 || !lambda || !u) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
-    Stage sf;
+    // host arrays cross PCIe once: u0 up, (lambda up when warm), lambda and u down
+    Stage sf, su0, sl, su;
     sf.ctx = ctx;
     sf.bytes = sizeof(double) * abi_nodes(ctx);
     sf.staged = true;   // a pooled device scratch for f (released by stage_finish)
     RC(stage_acquire(ctx, sf, sf.bytes));
-    int rc = wd_rhs(ctx, u0, sf.d, stream);
-    int rs = rc ? rc : wd_solve(ctx, sf.d, warm ? lambda : nullptr, rel_tol, lambda, rep, stream);
-    if (rs == WD_OK || rs == WD_E_NOCONV) rc = wd_recover_wind(ctx, lambda, u0, u, stream);
-    const int rf = stage_finish(st, {&sf});
+    RC(stage_in(ctx, su0, u0, abi_elems(ctx), st));
+    if (warm) RC(stage_in(ctx, sl, lambda, abi_nodes(ctx), st));
+    else RC(stage_out(ctx, sl, lambda, abi_nodes(ctx)));
+    sl.out = true;
+    sl.host = lambda;
+    RC(stage_out(ctx, su, u, abi_elems(ctx)));
+    int rc = wd_rhs(ctx, su0.d, sf.d, stream);
+    int rs = rc ? rc : wd_solve(ctx, sf.d, warm ? sl.d : nullptr, rel_tol, sl.d, rep, stream);
+    if (rs == WD_OK || rs == WD_E_NOCONV) rc = wd_recover_wind(ctx, sl.d, su0.d, su.d, stream);
+    const int rf = stage_finish(st, {&sf, &su0, &sl, &su});
     if (rs) return rs;
     return rc ? rc : rf;
 }

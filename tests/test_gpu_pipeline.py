@@ -191,3 +191,25 @@ def test_example_downscale_demo_runs():
         assert float(r[3]) <= 1e-8            # converged
         assert float(r[5]) < float(r[4])      # projected wind more mass-consistent than u0
     assert int(rows[1][1]) < int(rows[0][1])  # warm start needs fewer cycles
+
+
+def test_downscale_step_host_arrays(wd):
+    """wd_downscale_step on pinned host arrays (u0 staged once, lambda and u
+    copied back) equals the device-array call bit for bit, cold and warm."""
+    p = synth.small(device=DEV)
+    ctx = wd.wd_assemble(p.X, p.Y, p.Z, p.a)
+    lam_d = torch.zeros(ctx.node_shape, dtype=torch.float64, device=DEV)
+    u_d, r_d = wd.wd_downscale_step(ctx, p.u0, lam_d, warm=False, rel_tol=1e-9)
+    lam_h = torch.zeros(ctx.node_shape, dtype=torch.float64).pin_memory()
+    u_h = torch.empty(p.u0.shape, dtype=torch.float64).pin_memory()
+    u0_h = p.u0.cpu().pin_memory()
+    _, r_h = wd.wd_downscale_step(ctx, u0_h, lam_h, warm=False, rel_tol=1e-9, u=u_h)
+    torch.cuda.synchronize()
+    assert r_h["cycles"] == r_d["cycles"]
+    assert torch.equal(lam_h, lam_d.cpu()) and torch.equal(u_h, u_d.cpu())
+    u0b = (p.u0 * 1.01).contiguous()
+    _, r2d = wd.wd_downscale_step(ctx, u0b, lam_d, warm=True, rel_tol=1e-9)
+    _, r2h = wd.wd_downscale_step(ctx, u0b.cpu().pin_memory(), lam_h, warm=True, rel_tol=1e-9, u=u_h)
+    torch.cuda.synchronize()
+    assert r2h["cycles"] == r2d["cycles"] and torch.equal(lam_h, lam_d.cpu())
+    ctx.close()
