@@ -56,3 +56,20 @@ def test_product_and_oracle_share_nothing():
     assert "wd.h" not in txt and "wd_internal" not in txt
     txt = open(os.path.join(ROOT, "oracle", "__init__.py")).read()
     assert "paper_2101_08453_b200" not in txt.split('"""', 2)[2]
+
+
+def _build_c_demo(out):
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2101_08453_b200")
+    cmd = ["gcc", "-O2", "-std=c11", "-Wall", "-Werror", os.path.join(root, "examples", "c_api_demo.c"),
+           "-I" + os.path.join(root, "include"), "-L" + lib, "-lwd", "-Wl,-rpath," + lib, "-lm",
+           "-o", out]
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
+def test_c_api_demo_compiles_against_header(tmp_path):
+    """The boundary is a plain C library: a C program using only include/wd.h
+    compiles and links against libwd.so (no torch, no Python)."""
+    r = _build_c_demo(str(tmp_path / "c_api_demo"))
+    assert r.returncode == 0, r.stderr

@@ -213,3 +213,30 @@ def test_downscale_step_host_arrays(wd):
     torch.cuda.synchronize()
     assert r2h["cycles"] == r2d["cycles"] and torch.equal(lam_h, lam_d.cpu())
     ctx.close()
+
+
+def test_c_api_demo_runs(tmp_path):
+    """examples/c_api_demo.c (host arrays through the C ABI only): converges,
+    the projection lowers the weak divergence, and the lowest-layer vertical
+    wind is up on the windward and down on the lee side of the hill."""
+    import subprocess
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_abi import _build_c_demo
+    exe = str(tmp_path / "c_api_demo")
+    r = _build_c_demo(exe)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    vals = {}
+    for line in out.stdout.splitlines():
+        toks = line.replace("|", " ").split()
+        for a, b in zip(toks, toks[1:]):
+            try:
+                vals.setdefault(a, float(b))
+            except ValueError:
+                pass
+    assert vals["residual"] <= 1e-8
+    assert float(out.stdout.split("|D1 u| =")[1].split()[0]) < float(out.stdout.split("|D1 u0| =")[1].split()[0])
+    assert vals["windward"] > 0 and vals["lee"] < 0
