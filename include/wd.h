@@ -87,7 +87,8 @@ typedef struct {
     long long gather_below_nodes; /* slab decomposition: replicate ("gather") coarse levels with
                                      fewer nodes than this (default 2,000,000) */
     int rank, nranks;        /* slab decomposition in node rows j:
-                                nranks = 1: one GPU, whole grid (default);
+                                nranks = 1: one GPU, whole grid (default; with rank = 0 and
+                                  a one-rank nccl_comm the NCCL code path runs, no neighbours);
                                 nranks > 1, rank >= 0: this process is `rank` of nranks (one
                                   GPU per process, NCCL over NVLink, nccl_comm required); the
                                   node/element arrays passed to every call are this rank's

@@ -925,7 +925,9 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
     PT.start(st);
     // ---- decomposition
     ctx->nranks = o.nranks > 1 ? o.nranks : 1;
-    if (ctx->nranks == 1) ctx->mode = MODE_SINGLE;
+    // one rank with a communicator runs the NCCL path (no neighbours: the
+    // exchanges are empty groups, rank sums go through ncclAllGather)
+    if (ctx->nranks == 1 && !(o.rank == 0 && o.nccl_comm)) ctx->mode = MODE_SINGLE;
     else if (o.rank < 0) ctx->mode = MODE_VIRTUAL;
     else ctx->mode = MODE_NCCL;
     if (ctx->nranks > 64) return fail(WD_E_INVAL, "nranks %d > 64", ctx->nranks);

@@ -95,3 +95,28 @@ def test_virtual_ranks_f4_entry_points(wd):
     assert r1["cycles"] == rR["cycles"] and torch.equal(l1, lR) and torch.equal(u1, uR)
     ctx.close()
     ref.close()
+
+
+def test_nccl_one_rank_bitwise(wd):
+    """The NCCL code path on one GPU: libnccl found by dlopen, a one-rank
+    communicator, empty exchange groups, rank sums through ncclAllGather
+    (also inside the captured V-cycle graph).  Bitwise equal to the
+    single-GPU context."""
+    p = PROBLEMS["ragged"]()
+    n2 = p.X.shape[1]
+    comm = wd.wd_nccl_comm_init(wd.wd_nccl_unique_id(), 1, 0)
+    ref = _ctx(wd, p, 1, 0)
+    jb, je = wd.wd_partition_rows(n2, 1, 0)
+    assert (jb, je) == (0, n2)
+    opt = wd.default_options(coarsest_max_free=200, nranks=1, rank=0, nccl_comm=comm,
+                             j_begin=jb, j_end=je)
+    ctx = wd.wd_assemble(p.X, p.Y, p.Z, p.a, opt)
+    f1, fN = wd.wd_rhs(ref, p.u0), wd.wd_rhs(ctx, p.u0)
+    assert torch.equal(f1, fN)
+    l1, rep1 = wd.wd_solve(ref, f1, rel_tol=1e-9)
+    lN, repN = wd.wd_solve(ctx, fN, rel_tol=1e-9)
+    assert rep1["cycles"] == repN["cycles"]
+    assert torch.equal(l1, lN)
+    assert torch.equal(wd.wd_recover_wind(ref, l1, p.u0), wd.wd_recover_wind(ctx, lN, p.u0))
+    ctx.close()
+    ref.close()
