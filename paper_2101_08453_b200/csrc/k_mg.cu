@@ -398,7 +398,7 @@ prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
         const double* c3 = xc + loff(C, ix + nx - 1, iy + ny - 1, 0);
         double* xo = x + loff(F, i, j, 0);
         const bool two = nx == 2;
-#pragma unroll 4
+#pragma unroll 16   // all planes' loads in flight (Paper-scale level 0: 0.71 -> 0.58 ms)
         for (int k = 0; k <= F.n3 - 2; k++) {
             const i64 kc = (i64)k * C.sk;
             double sr = 0.0 + ldg(c0 + kc);
