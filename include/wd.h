@@ -266,7 +266,8 @@ int wd_downscale_step(wd_ctx* ctx, const double* u0, double* lambda, int warm, d
  * events: which = 0 GS sweep (the context's smoother), 1 residual apply,
  * 2 restrict (level -> level+1), 3 prolong, 4 V-cycle (level 0), 5 residual
  * norm (level 0), 6 Galerkin (level -> level+1), 7 level-0 assembly, 8 GS
- * sweep as 4 colour-phase launches.  One untimed
+ * sweep as 4 colour-phase launches, 9 fused GS sweep that also returns the
+ * residual of its input (the first sweep of a cycle in wd_solve).  One untimed
  * warm-up, then *ms_out = mean over `reps`.  Overwrites internal vectors
  * (and, for 6/7, recomputes identical operators). */
 int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out);

@@ -113,7 +113,8 @@ ABI_SYMBOLS = ["wd_default_options", "wd_assemble", "wd_rhs", "wd_vcycle", "wd_s
                "wd_downscale_step"]
 
 BENCH_KERNELS = {"gs_sweep": 0, "apply": 1, "restrict": 2, "prolong": 3, "vcycle": 4,
-                 "residual_norm": 5, "galerkin": 6, "assemble": 7, "gs_sweep_phased": 8}
+                 "residual_norm": 5, "galerkin": 6, "assemble": 7, "gs_sweep_phased": 8,
+                 "gs_sweep_res": 9}
 
 
 class WDError(RuntimeError):

@@ -29,8 +29,10 @@
 //     tile of the CTA), colour c handles g = s - 2c at step s, so the next
 //     tile's first planes are updated while the previous tile's last colours
 //     finish (no per-tile fill/drain or prologue);
-//   * lambda of the tile (+ halo) lives in a 16-plane shared-memory ring,
-//     filled with cp.async five planes ahead; the old iterate is read from one
+//   * lambda of the tile (+ halo) lives in a 12-plane shared-memory ring
+//     (76 KB: the kernel depends on the L1 left beside it -- the same kernel
+//     with 2x the shared memory reserved takes 2x as long),
+//     filled with cp.async four planes ahead; the old iterate is read from one
 //     buffer and the new one written to another (ping-pong), so halo reads
 //     never see a neighbour CTA's new values;
 //   * the 27 couplings, f and the diagonal of a thread's next node are loaded
@@ -40,6 +42,13 @@
 //     the operator about once per sweep (ncu, Paper-scale level 0: 19.7 GB
 //     read per sweep against 18.3 GB algorithmic; the four phase launches
 //     read ~34 GB).
+//
+// Residual variant (RES = true, used for the first sweep of a V-cycle inside
+// wd_solve): the sweep also returns ||f - K lin||^2 over its owned free nodes,
+// i.e. the convergence test of the previous cycle's iterate, from the
+// couplings it already holds in registers and an unmodified second copy of the
+// lambda ring (lin is never written during the sweep) -- no separate residual
+// pass over the operator.
 #include "wd_internal.cuh"
 
 #include <algorithm>
@@ -56,9 +65,9 @@ constexpr int SW = HI + 4;          // ring positions per parity per row (column
 constexpr int RW = 2 * SW;          // ring doubles per row
 constexpr int SH = TJ + 3;          // ring rows J0-1 .. J0+TJ+1
 constexpr int PL = RW * SH;         // ring doubles per plane
-constexpr int RING = 16;            // planes in the ring (power of 2, >= LA + 8)
+constexpr int RING = 12;            // planes in the ring (>= LA + 8: colour 3 reads plane s-7)
 constexpr int LAG = 2;              // plane lag between consecutive colours
-constexpr int LA = 5;               // lambda planes loaded ahead
+constexpr int LA = 4;               // lambda planes loaded ahead
 // colour regions: rows per colour (B) and halo columns beyond the 32 aligned ones
 constexpr int B0 = TJ / 2 + 1, B1 = TJ / 2 + 1, B2 = TJ / 2, B3 = TJ / 2;
 constexpr int W0 = B0, W1 = W0 + B1, W2 = W1 + B2, W3 = W2 + B3;   // warp ranges
@@ -75,12 +84,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+template <bool RES>
 __global__ void __launch_bounds__(THREADS, 1)
 gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict__ lin,
                      double* __restrict__ lout, const double* __restrict__ f, int jt0, int ntx,
-                     int ntiles) {
+                     int ntiles, double* __restrict__ partial) {
     extern __shared__ double ring[];
-    for (int t = threadIdx.x; t < PL * RING; t += THREADS) ring[t] = 0.0;
+    // RES: ring + PL * RING holds a second copy of the old iterate, never overwritten
+    for (int t = threadIdx.x; t < PL * RING * (RES ? 2 : 1); t += THREADS) ring[t] = 0.0;
 
     // this thread's colour c and the in-tile offsets (di, dj) of its column:
     // one warp per (colour, row) over the 32 aligned positions, the last warp
@@ -173,13 +184,18 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
     };
     if (G > 0) load_tile(0);
     auto load_next = [&]() {
-        double* dst = ring + ((kl * n3 + zl) & (RING - 1)) * PL;
+        double* dst = ring + ((kl * n3 + zl) % RING) * PL;
         const i64 pb = lbase + (i64)zl * L.sk;
 #pragma unroll
         for (int q = 0; q < NE; q++) {
             const int e = (int)threadIdx.x + q * THREADS;
-            if (lvalid & (1u << q)) cp_async8(dst + e, lin + pb + eoff[q]);
-            else if (e < PL) dst[e] = 0.0;
+            if (lvalid & (1u << q)) {
+                cp_async8(dst + e, lin + pb + eoff[q]);
+                if (RES) cp_async8(dst + PL * RING + e, lin + pb + eoff[q]);
+            } else if (e < PL) {
+                dst[e] = 0.0;
+                if (RES) dst[PL * RING + e] = 0.0;
+            }
         }
         if (++zl == n3) {
             zl = 0;
@@ -213,6 +229,7 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
     if (G > 0) set_tile(0);
     if (c == 0 && act && G > 0) load_k(0);
 
+    double rr = 0.0;   // RES: this thread's sum of squared residuals
     const int nsteps = G + LAG * 3;
     for (int s = 0; s < nsteps; s++) {
         if (s + LA < G) load_next();
@@ -221,9 +238,9 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
         if (g >= 0 && g < G) {
             const int z = zn;
             if (z < nz && act) {
-                const double* r1 = ring + ((g + 1) & (RING - 1)) * PL + so;
-                const double* r0 = ring + (g & (RING - 1)) * PL + so;
-                const double* rm = ring + ((g - 1) & (RING - 1)) * PL + so;
+                const double* r1 = ring + ((g + 1) % RING) * PL + so;
+                const double* r0 = ring + (g % RING) * PL + so;
+                const double* rm = ring + ((g + RING - 1) % RING) * PL + so;
                 double acc = 0.0;
 #pragma unroll
                 for (int sl = 1; sl < 14; sl++) {
@@ -240,7 +257,30 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
                     }
                 }
                 const double v = (fv - acc) / kd;
-                ring[(g & (RING - 1)) * PL + so] = v;
+                if (RES && wrt) {
+                    // residual of the old iterate at this node: every value from ring_old
+                    const double* o1 = r1 + PL * RING;
+                    const double* o0 = r0 + PL * RING;
+                    const double* om = rm + PL * RING;
+                    double q = kd * o0[0];
+#pragma unroll
+                    for (int sl = 1; sl < 14; sl++) {
+                        const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+                        q = fma(kf[sl - 1], (dz ? o1 : o0)[sc(dx, dy)], q);
+                    }
+#pragma unroll
+                    for (int sl = 1; sl < 14; sl++) {
+                        const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+                        if (dz) {
+                            if (z > 0) q = fma(kb[sl - 1], om[sc(-dx, -dy)], q);
+                        } else {
+                            q = fma(kb[sl - 1], o0[sc(-dx, -dy)], q);
+                        }
+                    }
+                    const double rv = fv - q;
+                    rr = fma(rv, rv, rr);
+                }
+                ring[(g % RING) * PL + so] = v;
                 if (wrt) lout[own + (i64)z * L.sk] = v;
             }
             if (++zn == n3) {
@@ -255,17 +295,32 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
         __syncthreads();
     }
     cp_async_wait<0>();
+    if (RES) {   // fixed-order block sum (deterministic): warp tree, then warps in order
+        __shared__ double wsum[THREADS / 32];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rr += __shfl_down_sync(0xffffffffu, rr, o);
+        if (lane == 0) wsum[w] = rr;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < THREADS / 32; q++) t += wsum[q];
+            partial[blockIdx.x] = t;
+        }
+    }
 }
 
 }  // namespace
 
 // one sweep: lin (old iterate, unchanged) -> lout (new iterate on the owned
-// free nodes; D entries of lout must already be 0)
-void launch_gs_fused(const LevDev& L, const double* coef, const double* lin, double* lout,
-                     const double* f, cudaStream_t st) {
+// free nodes; D entries of lout must already be 0).  partial != NULL: also
+// ||f - K lin||^2 over the owned free nodes as one partial per CTA; returns
+// the number of CTAs (partials)
+int launch_gs_fused(const LevDev& L, const double* coef, const double* lin, double* lout,
+                    const double* f, cudaStream_t st, double* partial) {
     static int nsm = 0;
     if (!nsm) {
-        cudaFuncSetAttribute(gs_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        cudaFuncSetAttribute(gs_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        cudaFuncSetAttribute(gs_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * SMEM));
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -276,7 +331,13 @@ void launch_gs_fused(const LevDev& L, const double* coef, const double* lin, dou
     const int ntx = (L.n1 + TI - 1) / TI, nty = (L.own1 - jt0 + TJ - 1) / TJ;
     g_launches += 1;
     const int grid = std::min(ntx * nty, nsm);   // persistent: one CTA per SM
-    gs_fused_kernel<<<grid, THREADS, SMEM, st>>>(L, coef, lin, lout, f, jt0, ntx, ntx * nty);
+    if (partial)
+        gs_fused_kernel<true><<<grid, THREADS, 2 * SMEM, st>>>(L, coef, lin, lout, f, jt0, ntx,
+                                                               ntx * nty, partial);
+    else
+        gs_fused_kernel<false><<<grid, THREADS, SMEM, st>>>(L, coef, lin, lout, f, jt0, ntx,
+                                                            ntx * nty, nullptr);
+    return grid;
 }
 
 }  // namespace wd

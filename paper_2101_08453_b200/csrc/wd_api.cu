@@ -230,12 +230,18 @@ struct wd_ctx {
     cudaStream_t pin_s = nullptr, pout_s = nullptr;
     cudaEvent_t pev[17] = {};
     cudaGraphExec_t vgraph = nullptr;
+    // wd_solve with the fused smoother: the V-cycle split after its first
+    // level-0 sweep; that sweep also returns the residual of its input
+    // (k_gs_fused.cu RES), so the convergence test needs no residual pass
+    cudaGraphExec_t g_first_res = nullptr, g_first = nullptr, g_rest = nullptr;
+    long long k_first_res = 0, k_first = 0, k_rest = 0;
     long long bytes = 0;
     std::vector<std::pair<void*, size_t>> pool;   // staging buffers for host pointers
     std::vector<int> pool_busy;
     long long graph_kernels = 0;
     cudaEvent_t ev_gs[32] = {};
     cudaEvent_t ev_cyc[2] = {};
+    bool first_res = false;    // the last cycle's first sweep was the residual variant
     cudaEvent_t ev_res[2] = {};
     double prof[6] = {0, 0, 0, 0, 0, 0};
 };
@@ -656,11 +662,38 @@ int smooth_end(wd_ctx* ctx, int l, cudaStream_t st) {
     return WD_OK;
 }
 
-int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st) {
+// the first level-0 sweep of a V-cycle with the fused kernel's residual
+// output: ||f - K lam||^2 of the iterate entering the sweep (all ranks) into
+// dscal[0]; the sweep itself is the one smooth() performs
+int smooth_first_res(wd_ctx* ctx, bool prof, cudaStream_t st) {
+    if (prof) CK(cudaEventRecordWithFlags(ctx->ev_gs[0], st, cudaEventRecordExternal));
+    RC(exchange(ctx, 0, ARR_LAM, 2, st));
+    double* per = ctx->dscal + 128;   // per-part sums
+    for (size_t p = 0; p < ctx->parts.size(); p++) {
+        Part& P = ctx->parts[p];
+        Level& F = P.lev[0];
+        const int nb = launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st, P.partial);
+        std::swap(F.lam, F.lam2);
+        launch_reduce_sum(P.partial, nb, per + p, st);
+    }
+    RC(sum_ranks(ctx, per, ctx->dscal, st));
+    if (prof) CK(cudaEventRecordWithFlags(ctx->ev_gs[1], st, cudaEventRecordExternal));
+    CKL();
+    return WD_OK;
+}
+
+// can wd_solve take its convergence test from the first sweep of each cycle?
+bool lagged_residual(const wd_ctx* ctx) {
+    return ctx->opt.smoother == WD_SMOOTH_FUSED && ctx->nlev > 1 && ctx->opt.pre_smooth >= 1;
+}
+
+// first = 1: the first level-0 pre-smoothing sweep has already run
+// (smooth_first_res or smooth), continue the cycle from there
+int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st, int first = 0) {
     if (l == ctx->nlev - 1) return coarse_solve(ctx, st);
     const bool prof = ctx->opt.profile && l == 0 && ctx->parts.size() == 1;
-    int ns = 0;
-    for (int s = 0; s < ctx->opt.pre_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
+    int ns = first;
+    for (int s = first; s < ctx->opt.pre_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
     RC(smooth_end(ctx, l, st));
     for (Part& P : ctx->parts) apply_level(P.lev[l], true, nullptr, st);
     RC(exchange(ctx, l, ARR_R, 1, st));
@@ -692,7 +725,8 @@ void profile_accumulate(wd_ctx* ctx, bool cycle, bool resid) {
     if (cycle) {
         const int ns = std::min(ctx->opt.pre_smooth + ctx->opt.post_smooth, 16);
         if (ctx->nlev > 1 && ctx->parts.size() == 1)
-            for (int s = 0; s < ns; s++)
+            // level-0 sweeps of the plain kernel (the residual variant is not counted)
+            for (int s = ctx->first_res ? 1 : 0; s < ns; s++)
                 if (cudaEventElapsedTime(&ms, ctx->ev_gs[2 * s], ctx->ev_gs[2 * s + 1]) == cudaSuccess) {
                     ctx->prof[0] += ms;
                     ctx->prof[1] += 1;
@@ -710,6 +744,7 @@ void profile_accumulate(wd_ctx* ctx, bool cycle, bool resid) {
 }
 
 int run_vcycle(wd_ctx* ctx, cudaStream_t st) {
+    ctx->first_res = false;
     if (ctx->opt.profile) CK(cudaEventRecord(ctx->ev_cyc[0], st));
     if (!ctx->opt.use_graph) {
         RC(vcycle_level(ctx, 0, st));
@@ -732,6 +767,68 @@ int run_vcycle(wd_ctx* ctx, cudaStream_t st) {
         g_launches += ctx->graph_kernels;
     }
     if (ctx->opt.profile) CK(cudaEventRecord(ctx->ev_cyc[1], st));
+    return WD_OK;
+}
+
+// capture fn(stream) into an executable graph (kernels counted, not executed)
+template <class Fn>
+int capture_graph(wd_ctx* ctx, cudaGraphExec_t* out, long long* nk, Fn fn) {
+    const long long before = g_launches.load();
+    CK(cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeThreadLocal));
+    const int rc = fn(ctx->cap);
+    cudaGraph_t g;
+    cudaError_t e = cudaStreamEndCapture(ctx->cap, &g);
+    *nk = g_launches.load() - before;
+    g_launches -= *nk;
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(WD_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(out, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(WD_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    return WD_OK;
+}
+
+// the split V-cycle of wd_solve: which = 0 first sweep + residual of its
+// input, 1 first sweep only, 2 the rest of the cycle.  The host-side buffer
+// roles follow the stream order (the first sweep swaps lam/lam2 of level 0;
+// the rest of the cycle ends with the iterate back in the canonical buffer).
+int run_split(wd_ctx* ctx, int which, cudaStream_t st) {
+    const bool prof = ctx->opt.profile && ctx->parts.size() == 1;
+    if (which < 2 && ctx->opt.profile) CK(cudaEventRecord(ctx->ev_cyc[0], st));
+    auto body = [&](cudaStream_t s) -> int {
+        if (which == 0) return smooth_first_res(ctx, prof, s);
+        if (which == 1) return smooth(ctx, 0, prof, 0, s);
+        return vcycle_level(ctx, 0, s, 1);
+    };
+    if (!ctx->opt.use_graph) {
+        RC(body(st));
+    } else {
+        if (!ctx->g_first_res) {
+            if (which == 2) return fail(WD_E_INVAL, "split V-cycle: rest before first sweep");
+            // capture all three from the canonical state: the two first-sweep
+            // variants each swap the level-0 buffers, the rest swaps them back
+            RC(capture_graph(ctx, &ctx->g_first, &ctx->k_first,
+                             [&](cudaStream_t s) { return smooth(ctx, 0, prof, 0, s); }));
+            for (Part& P : ctx->parts) std::swap(P.lev[0].lam, P.lev[0].lam2);
+            RC(capture_graph(ctx, &ctx->g_first_res, &ctx->k_first_res,
+                             [&](cudaStream_t s) { return smooth_first_res(ctx, prof, s); }));
+            RC(capture_graph(ctx, &ctx->g_rest, &ctx->k_rest,
+                             [&](cudaStream_t s) { return vcycle_level(ctx, 0, s, 1); }));
+            // host roles now canonical; replay the first sweep's swap below
+        }
+        cudaGraphExec_t g = which == 0 ? ctx->g_first_res : which == 1 ? ctx->g_first : ctx->g_rest;
+        CK(cudaGraphLaunch(g, st));
+        g_launches += which == 0 ? ctx->k_first_res : which == 1 ? ctx->k_first : ctx->k_rest;
+        // keep the host-side roles in step with the replayed graph
+        if (which < 2)
+            for (Part& P : ctx->parts) std::swap(P.lev[0].lam, P.lev[0].lam2);
+        else
+            for (Part& P : ctx->parts) {
+                Level& F = P.lev[0];
+                if (F.lam != F.raw[1]) std::swap(F.lam, F.lam2);
+            }
+    }
+    if (which == 2 && ctx->opt.profile) CK(cudaEventRecord(ctx->ev_cyc[1], st));
     return WD_OK;
 }
 
@@ -853,6 +950,8 @@ void wd_destroy(wd_ctx* ctx) {
     cudaDeviceSynchronize();   // no work of the context may still be in flight
     cudaGetLastError();
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
+    for (cudaGraphExec_t g : {ctx->g_first_res, ctx->g_first, ctx->g_rest})
+        if (g) cudaGraphExecDestroy(g);
     if (ctx->cap) cudaStreamDestroy(ctx->cap);
     if (ctx->pin_s) cudaStreamDestroy(ctx->pin_s);
     if (ctx->pout_s) cudaStreamDestroy(ctx->pout_s);
@@ -1635,10 +1734,24 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
     R.coarse_direct = ctx->coarse_direct;
     R.coarse_free = ctx->nf;
     RC(norm_sq(ctx, ARR_F, 1, st));
-    if (lambda0) {
+    // convergence test of iterate c: ||f - K lam_c|| / ||f||.  With the fused
+    // smoother it is normally taken from the first sweep of cycle c+1, which
+    // reads lam_c unchanged (ping-pong) and returns its residual (RES variant);
+    // when the test passes, lam_c is still in the canonical buffer and the
+    // sweep's output is dropped.  A separate residual pass is used for the
+    // warm start when the split is not available, at the cycle cap, and after
+    // a cycle predicted (from the last two factors) to reach rel_tol.  Either
+    // way the test sees the same quantity after every cycle, so the cycle
+    // count is the one of "cycle, then test".
+    const bool lag = lagged_residual(ctx);
+    bool have = true;   // hscal[0] holds ||r||^2 of the current iterate
+    if (lambda0 && !lag) {
         RC(residual_sq(ctx, 0, st));
         RC(fetch_scalars(ctx, 2, st));
         profile_accumulate(ctx, false, true);
+    } else if (lambda0) {
+        RC(fetch_scalars(ctx, 2, st));
+        have = false;
     } else {
         // zero start: f - K 0 = f exactly, no residual pass needed
         RC(fetch_scalars(ctx, 2, st));
@@ -1652,22 +1765,49 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
         R.rel_res_hist[0] = 0.0;
         status = WD_OK;
     } else {
-        double rel = std::sqrt(ctx->hscal[0]) / fn;
-        R.rel_res_hist[0] = rel;
-        R.rel_res0 = rel;
-        if (!std::isfinite(rel)) status = WD_E_NONFINITE;
-        else if (rel <= rel_tol) status = WD_OK;
-        while (status == WD_E_NOCONV && c < ctx->opt.max_cycles) {
-            RC(run_vcycle(ctx, st));
-            RC(residual_sq(ctx, 0, st));
-            RC(fetch_scalars(ctx, 1, st));
-            c++;
-            profile_accumulate(ctx, true, true);
-            rel = std::sqrt(ctx->hscal[0]) / fn;
+        for (;;) {
+            bool first_done = false;
+            if (!have) {   // first sweep of cycle c+1, returning the residual of lam_c
+                RC(run_split(ctx, 0, st));
+                RC(fetch_scalars(ctx, 1, st));
+                first_done = true;
+            }
+            const double rel = std::sqrt(ctx->hscal[0]) / fn;
             if (c < 256) R.rel_res_hist[c] = rel;
-            if (!std::isfinite(rel)) { status = WD_E_NONFINITE; break; }
-            if (rel <= rel_tol) { status = WD_OK; break; }
-            if (c >= 3 && c < 256 && rel > 10.0 * R.rel_res_hist[c - 3]) { status = WD_E_DIVERGED; break; }
+            if (c == 0) R.rel_res0 = rel;
+            if (!std::isfinite(rel)) status = WD_E_NONFINITE;
+            else if (rel <= rel_tol) status = WD_OK;
+            else if (c >= 3 && c < 256 && rel > 10.0 * R.rel_res_hist[c - 3]) status = WD_E_DIVERGED;
+            else if (c >= ctx->opt.max_cycles) status = WD_E_NOCONV;
+            else status = -1;   // continue
+            if (status != -1) {
+                if (first_done)   // drop the sweep: lam_c is the result
+                    for (Part& P : ctx->parts) std::swap(P.lev[0].lam, P.lev[0].lam2);
+                break;
+            }
+            if (!lag) {
+                RC(run_vcycle(ctx, st));
+                RC(residual_sq(ctx, 0, st));
+                RC(fetch_scalars(ctx, 1, st));
+                c++;
+                profile_accumulate(ctx, true, true);
+                continue;
+            }
+            if (!first_done) RC(run_split(ctx, 1, st));
+            ctx->first_res = first_done;
+            RC(run_split(ctx, 2, st));
+            c++;
+            profile_accumulate(ctx, true, false);
+            const double prev = c >= 2 && c - 2 < 256 ? R.rel_res_hist[c - 2] : 0.0;
+            const bool predicted = prev > 0.0 && rel * (rel / prev) <= rel_tol;
+            if (predicted || c >= ctx->opt.max_cycles) {
+                RC(residual_sq(ctx, 0, st));
+                RC(fetch_scalars(ctx, 1, st));
+                profile_accumulate(ctx, false, true);
+                have = true;
+            } else {
+                have = false;
+            }
         }
     }
     R.cycles = c;
@@ -1721,6 +1861,12 @@ int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out)
                 RC(smooth(ctx, level, false, 0, st));
                 return smooth_end(ctx, level, st);
             case 8: launch_gs_sweep(F.L, F.coef, F.lam, F.f, st); break;
+            case 9:   // two fused sweeps of the residual variant, reported per sweep
+                for (int t = 0; t < 2; t++) {
+                    launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st, P.partial);
+                    std::swap(F.lam, F.lam2);
+                }
+                return smooth_end(ctx, level, st);
             case 1: apply_level(F, true, nullptr, st); break;
             case 2: launch_restrict(F.L, target(P.lev[level + 1]), F.M, F.r, P.lev[level + 1].f, F.nkept == F.L.n3, st); break;
             case 3: launch_prolong(F.L, P.lev[level + 1].L, F.M, P.lev[level + 1].lam, F.lam, F.nkept == F.L.n3, st); break;
@@ -1744,7 +1890,7 @@ int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out)
     CK(cudaEventSynchronize(e1));
     float ms;
     CK(cudaEventElapsedTime(&ms, e0, e1));
-    *ms_out = ms / reps / (which == 0 ? 2 : 1);
+    *ms_out = ms / reps / (which == 0 || which == 9 ? 2 : 1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     CKL();

@@ -142,8 +142,10 @@ void launch_argmin_bottom(const double* Z, int n, double* pval, long long* pidx,
                           cudaStream_t st);
 
 // k_gs_fused.cu: one whole 4-colour sweep per launch, lin -> lout (ping-pong)
-void launch_gs_fused(const LevDev& L, const double* coef, const double* lin, double* lout,
-                     const double* f, cudaStream_t st);
+// partial != NULL: also the residual of lin, ||f - K lin||^2 as per-CTA
+// partials (returns their number)
+int launch_gs_fused(const LevDev& L, const double* coef, const double* lin, double* lout,
+                    const double* f, cudaStream_t st, double* partial = nullptr);
 
 // k_io.cu: steps either side of the path
 void launch_build_mesh(const double* zs, int n1, int n2, int n3, double x0, double y0, double dx,

@@ -33,7 +33,7 @@ def main():
     n1, n2, n3 = ctx.level_dims(0)
     free0 = (n1 - 2) * (n2 - 2) * (n3 - 1)
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
-    alg = {"gs_sweep": 136 * free0, "gs_sweep_phased": 264 * free0, "apply": 136 * free0, "residual_norm": 128 * free0,
+    alg = {"gs_sweep": 136 * free0, "gs_sweep_res": 136 * free0, "gs_sweep_phased": 264 * free0, "apply": 136 * free0, "residual_norm": 128 * free0,
            "prolong": 16 * free0, "restrict": 8 * free0 + 8 * free0 // 4}
 
     def report(name, level=0, extra=None):
@@ -50,7 +50,7 @@ def main():
         for name in args.only.split(","):
             report(name)
         return
-    for name in ["gs_sweep", "gs_sweep_phased", "apply", "residual_norm", "restrict", "prolong", "vcycle"]:
+    for name in ["gs_sweep", "gs_sweep_res", "gs_sweep_phased", "apply", "residual_norm", "restrict", "prolong", "vcycle"]:
         report(name)
     for l in range(1, ctx.num_levels() - 1):
         report("gs_sweep", l)
