@@ -46,9 +46,9 @@
 // Residual variant (RES = true, used for the first sweep of a V-cycle inside
 // wd_solve): the sweep also returns ||f - K lin||^2 over its owned free nodes,
 // i.e. the convergence test of the previous cycle's iterate, from the
-// couplings it already holds in registers and an unmodified second copy of the
-// lambda ring (lin is never written during the sweep) -- no separate residual
-// pass over the operator.
+// couplings it already holds in registers; old values of neighbours already
+// updated come from an 8-plane shadow where each thread saves its node's old
+// value when it overwrites it -- no separate residual pass over the operator.
 #include "wd_internal.cuh"
 
 #include <algorithm>
@@ -74,6 +74,10 @@ constexpr int W0 = B0, W1 = W0 + B1, W2 = W1 + B2, W3 = W2 + B3;   // warp range
 constexpr int NHALO = 3 * B0 + 2 * B1 + B2;                          // 29 halo columns
 constexpr int THREADS = 32 * (W3 + 1);                               // 19 warps
 constexpr size_t SMEM = sizeof(double) * PL * RING;
+// residual variant: a node of colour c' is overwritten at step z + 2c' and its
+// old value read by higher colours up to plane z + 1 at step z + 1 + 6
+constexpr int SHADOW = 8;
+constexpr size_t SMEM_RES = SMEM + sizeof(double) * PL * SHADOW;
 static_assert(NHALO <= 32, "halo columns must fit one warp");
 
 __device__ __forceinline__ void cp_async8(double* s, const double* g) {
@@ -90,8 +94,10 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
                      double* __restrict__ lout, const double* __restrict__ f, int jt0, int ntx,
                      int ntiles, double* __restrict__ partial) {
     extern __shared__ double ring[];
-    // RES: ring + PL * RING holds a second copy of the old iterate, never overwritten
-    for (int t = threadIdx.x; t < PL * RING * (RES ? 2 : 1); t += THREADS) ring[t] = 0.0;
+    // RES: the old values of the last SHADOW planes, saved by each thread when
+    // it overwrites its node in the ring
+    double* shadow = ring + PL * RING;
+    for (int t = threadIdx.x; t < PL * (RING + (RES ? SHADOW : 0)); t += THREADS) ring[t] = 0.0;
 
     // this thread's colour c and the in-tile offsets (di, dj) of its column:
     // one warp per (colour, row) over the 32 aligned positions, the last warp
@@ -189,13 +195,8 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
 #pragma unroll
         for (int q = 0; q < NE; q++) {
             const int e = (int)threadIdx.x + q * THREADS;
-            if (lvalid & (1u << q)) {
-                cp_async8(dst + e, lin + pb + eoff[q]);
-                if (RES) cp_async8(dst + PL * RING + e, lin + pb + eoff[q]);
-            } else if (e < PL) {
-                dst[e] = 0.0;
-                if (RES) dst[PL * RING + e] = 0.0;
-            }
+            if (lvalid & (1u << q)) cp_async8(dst + e, lin + pb + eoff[q]);
+            else if (e < PL) dst[e] = 0.0;
         }
         if (++zl == n3) {
             zl = 0;
@@ -237,6 +238,9 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
         const int g = s - LAG * c;
         if (g >= 0 && g < G) {
             const int z = zn;
+            // RES: every mapped column saves its old value (also Dirichlet and
+            // outside-grid columns, which are never updated) before the update
+            if (RES && inreg) shadow[(g & (SHADOW - 1)) * PL + so] = ring[(g % RING) * PL + so];
             if (z < nz && act) {
                 const double* r1 = ring + ((g + 1) % RING) * PL + so;
                 const double* r0 = ring + (g % RING) * PL + so;
@@ -258,23 +262,34 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
                 }
                 const double v = (fv - acc) / kd;
                 if (RES && wrt) {
-                    // residual of the old iterate at this node: every value from ring_old
-                    const double* o1 = r1 + PL * RING;
-                    const double* o0 = r0 + PL * RING;
-                    const double* om = rm + PL * RING;
-                    double q = kd * o0[0];
+                    // residual of the old iterate at this node.  Neighbours of a
+                    // lower colour (c' < c, any plane) and the node below in the
+                    // column are already overwritten in the ring: their old values
+                    // are in the shadow.  c' = c ^ (dx odd) ^ 2 (dy odd), so
+                    // c' < c iff c is odd (dx odd, dy even) or c >= 2 (dy odd).
+                    const bool codd = c & 1, chi = c >= 2;
+                    const double* s1 = shadow + ((g + 1) & (SHADOW - 1)) * PL + so;
+                    const double* s0 = shadow + (g & (SHADOW - 1)) * PL + so;
+                    const double* sm = shadow + ((g + SHADOW - 1) & (SHADOW - 1)) * PL + so;
+                    auto oldv = [&](int dx, int dy, int dz) {
+                        const bool sh = (dx == 0 && dy == 0) ? dz < 0 : ((dy & 1) ? chi : codd);
+                        const double* rp = dz > 0 ? r1 : dz < 0 ? rm : r0;
+                        const double* sp = dz > 0 ? s1 : dz < 0 ? sm : s0;
+                        return (sh ? sp : rp)[sc(dx, dy)];
+                    };
+                    double q = kd * r0[0];   // own old value (overwritten below)
 #pragma unroll
                     for (int sl = 1; sl < 14; sl++) {
                         const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
-                        q = fma(kf[sl - 1], (dz ? o1 : o0)[sc(dx, dy)], q);
+                        q = fma(kf[sl - 1], oldv(dx, dy, dz), q);
                     }
 #pragma unroll
                     for (int sl = 1; sl < 14; sl++) {
                         const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
                         if (dz) {
-                            if (z > 0) q = fma(kb[sl - 1], om[sc(-dx, -dy)], q);
+                            if (z > 0) q = fma(kb[sl - 1], oldv(-dx, -dy, -dz), q);
                         } else {
-                            q = fma(kb[sl - 1], o0[sc(-dx, -dy)], q);
+                            q = fma(kb[sl - 1], oldv(-dx, -dy, 0), q);
                         }
                     }
                     const double rv = fv - q;
@@ -320,7 +335,7 @@ int launch_gs_fused(const LevDev& L, const double* coef, const double* lin, doub
     static int nsm = 0;
     if (!nsm) {
         cudaFuncSetAttribute(gs_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        cudaFuncSetAttribute(gs_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * SMEM));
+        cudaFuncSetAttribute(gs_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RES);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -332,7 +347,7 @@ int launch_gs_fused(const LevDev& L, const double* coef, const double* lin, doub
     g_launches += 1;
     const int grid = std::min(ntx * nty, nsm);   // persistent: one CTA per SM
     if (partial)
-        gs_fused_kernel<true><<<grid, THREADS, 2 * SMEM, st>>>(L, coef, lin, lout, f, jt0, ntx,
+        gs_fused_kernel<true><<<grid, THREADS, SMEM_RES, st>>>(L, coef, lin, lout, f, jt0, ntx,
                                                                ntx * nty, partial);
     else
         gs_fused_kernel<false><<<grid, THREADS, SMEM, st>>>(L, coef, lin, lout, f, jt0, ntx,

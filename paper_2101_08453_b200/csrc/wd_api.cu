@@ -721,6 +721,10 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st, int first = 0) {
 
 void profile_accumulate(wd_ctx* ctx, bool cycle, bool resid) {
     if (!ctx->opt.profile) return;
+    // the split V-cycle of wd_solve reaches here before any stream sync: wait
+    // for the events (profile mode only)
+    if (cycle) cudaEventSynchronize(ctx->ev_cyc[1]);
+    if (resid) cudaEventSynchronize(ctx->ev_res[1]);
     float ms;
     if (cycle) {
         const int ns = std::min(ctx->opt.pre_smooth + ctx->opt.post_smooth, 16);
