@@ -84,6 +84,10 @@ __device__ __forceinline__ void cp_async8(double* s, const double* g) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g) : "memory");
 }
+__device__ __forceinline__ void cp_async16(double* s, const double* g) {   // bypasses L1
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -161,12 +165,18 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
     // ring entries e = threadIdx.x + q THREADS (q < NE) of every plane; their
     // offsets relative to the tile origin are fixed, so per plane only the
     // tile base and the plane stride change.
-    constexpr int NE = (PL + THREADS - 1) / THREADS;
-    i64 eoff[NE];
-    int eri[NE], erj[NE];
+    // Entries go in pairs (2e, 2e+1: adjacent positions of one half row, 16 B
+    // aligned in HBM and in the ring) copied with one 16-byte cp.async.cg that
+    // bypasses L1 (the kernel lives on L1 hits of the couplings); a pair
+    // straddling the grid edge is copied or zeroed entry by entry.
+    constexpr int NE = (PL / 2 + THREADS - 1) / THREADS;   // pairs per thread
+    constexpr int NEL = 2 * NE;
+    static_assert(RW % 2 == 0 && SW % 2 == 0, "pairs must not straddle half rows");
+    i64 eoff[NEL];
+    int eri[NEL], erj[NEL];
 #pragma unroll
-    for (int q = 0; q < NE; q++) {
-        const int e = (int)threadIdx.x + q * THREADS;
+    for (int q = 0; q < NEL; q++) {
+        const int e = 2 * ((int)threadIdx.x + (q >> 1) * THREADS) + (q & 1);
         const int rj = e / RW, r = e - rj * RW;
         const int half = r >= SW, pos = r - half * SW;
         erj[q] = e < PL ? rj : -1000000;   // never valid beyond the ring
@@ -176,14 +186,14 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
     }
     int kl = 0, zl = 0;
     i64 lbase = 0;        // loff(I0 - 4 (even part), J0 - 1, zl) of the loading tile
-    unsigned lvalid = 0;  // bit q: entry q lies inside the grid
+    unsigned lvalid = 0;  // bit q: entry q lies inside the grid (NEL <= 32)
     auto load_tile = [&](int k) {
         int I0, J0;
         origin(k, I0, J0);
         lbase = (i64)(J0 - 1) * L.sj + (I0 >> 1) - 2;
         lvalid = 0;
 #pragma unroll
-        for (int q = 0; q < NE; q++) {
+        for (int q = 0; q < NEL; q++) {
             const int i = I0 - 4 + eri[q], j = J0 - 1 + erj[q];
             if (eri[q] >= 1 && i >= 0 && i < L.n1 && j >= 0 && j < L.n2) lvalid |= 1u << q;
         }
@@ -194,9 +204,15 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
         const i64 pb = lbase + (i64)zl * L.sk;
 #pragma unroll
         for (int q = 0; q < NE; q++) {
-            const int e = (int)threadIdx.x + q * THREADS;
-            if (lvalid & (1u << q)) cp_async8(dst + e, lin + pb + eoff[q]);
-            else if (e < PL) dst[e] = 0.0;
+            const int e = 2 * ((int)threadIdx.x + q * THREADS);
+            const unsigned b = (lvalid >> (2 * q)) & 3u;
+            if (b == 3u) cp_async16(dst + e, lin + pb + eoff[2 * q]);
+            else if (e < PL) {
+                if (b & 1u) cp_async8(dst + e, lin + pb + eoff[2 * q]);
+                else dst[e] = 0.0;
+                if (b & 2u) cp_async8(dst + e + 1, lin + pb + eoff[2 * q + 1]);
+                else dst[e + 1] = 0.0;
+            }
         }
         if (++zl == n3) {
             zl = 0;
