@@ -9,4 +9,6 @@ CMD="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --warm 0"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gs_fused_kernel -c 1 -o gpurun_out/prof_fused $CMD > gpurun_out/ncu_fused.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:apply_tma_kernel -c 1 -o gpurun_out/prof_apply $CMD > gpurun_out/ncu_apply.log 2>&1
+# the residual variant of the fused sweep (first sweep of a cycle in wd_solve)
+timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:gs_fused_kernel<true>' -c 1 -o gpurun_out/prof_fused_res $CMD > gpurun_out/ncu_fused_res.log 2>&1
 echo done >> gpurun_out/smoke.log

@@ -2,7 +2,7 @@
 """Summarise ncu output brought back in gpurun_out/ into profiles/ (tracked).
 
   python scripts/ncu_summary.py launches <launches.csv> <out.txt>
-  python scripts/ncu_summary.py full <prof.ncu-rep> <out.txt> [--traffic-key CONFIG]
+  python scripts/ncu_summary.py full <prof.ncu-rep> <out.txt> [--traffic-key KERNEL:CONFIG]
 
 `launches`: per-kernel totals / shares of a `--metrics gpu__time_duration.sum`
 launch list (cold-cache, serialised: compare shares, not absolutes).
