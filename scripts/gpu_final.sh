@@ -10,5 +10,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gs_fused_kernel -c 1 -o gpurun_out/prof_fused $CMD > gpurun_out/ncu_fused.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:apply_tma_kernel -c 1 -o gpurun_out/prof_apply $CMD > gpurun_out/ncu_apply.log 2>&1
 # the residual variant of the fused sweep (first sweep of a cycle in wd_solve)
-timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:gs_fused_kernel<true>' -c 1 -o gpurun_out/prof_fused_res $CMD > gpurun_out/ncu_fused_res.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:gs_fused_kernel<.bool.1>' -c 1 -o gpurun_out/prof_fused_res $CMD > gpurun_out/ncu_fused_res.log 2>&1
 echo done >> gpurun_out/smoke.log
