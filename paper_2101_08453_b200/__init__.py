@@ -165,13 +165,14 @@ class Context:
         self.dims = dims        # global node dims (n1, n2, n3)
         self.device = device
         self.rows = rows if rows is not None else dims[1]   # node rows of the ABI arrays
+        self._destroy = _lib.wd_destroy   # module globals may be gone at interpreter exit
 
     def __del__(self):
         self.close()
 
     def close(self):
         if getattr(self, "h", None):
-            _lib.wd_destroy(self.h)
+            self._destroy(self.h)
             self.h = None
 
     @property

@@ -481,13 +481,85 @@ __device__ __forceinline__ double galerkin_regular(const LevDev& F, const double
     return s;
 }
 
+// z pair list of the Galerkin product for coarse plane Kc and offset DZ (the
+// generic loop's construction: u major, v minor, |q - p| <= 1)
+__device__ __forceinline__ int zpairs(const MapDev& M, int fn3, int Kc, int DZ, int (&lt)[9],
+                                      int (&ld)[9], double (&lw)[9]) {
+    int pt[3], qt[3];
+    double pw[3], qw[3];
+    const int pm = support1d(M.pos[2], M.co[2], fn3, Kc, pt, pw);
+    const int qm = support1d(M.pos[2], M.co[2], fn3, Kc + DZ, qt, qw);
+    int n = 0;
+    for (int u = 0; u < pm; u++)
+        for (int v = 0; v < qm; v++) {
+            const int dd = qt[v] - pt[u];
+            if (dd >= -1 && dd <= 1) {
+                lt[n] = pt[u];
+                ld[n] = dd;
+                lw[n] = pw[u] * qw[v];
+                n++;
+            }
+        }
+    return n;
+}
+
+// K_c(I, I + (DX, DY, DZ)) for a coarse node with regular x and y supports on a
+// transition that merges layers (z map not the identity): x and y unrolled
+// with compile-time offsets, z pairs from zpairs(); the generic loop's
+// products and sums in its order (bitwise equal)
+template <int DX, int DY>
+__device__ __forceinline__ double galerkin_xyreg(const LevDev& F, const double* __restrict__ K,
+                                                 int fi, int fj, const int (&lt)[9],
+                                                 const int (&ld)[9], const double (&lw)[9], int ln) {
+    double s = 0.0;
+    for (int c = 0; c < ln; c++) {
+        const int k = lt[c], dz = ld[c];
+#pragma unroll
+        for (int b = 0; b < npairs<DY>(); b++) {
+            const Pair1 py = pair<DY>(b);
+            double sr = 0.0;
+#pragma unroll
+            for (int a = 0; a < npairs<DX>(); a++) {
+                const Pair1 px = pair<DX>(a);
+                sr = fma(px.w, kget(F, K, fi + px.u, fj + py.u, k, px.v - px.u, py.v - py.u, dz), sr);
+            }
+            s = fma(lw[c] * py.w, sr, s);
+        }
+    }
+    return s;
+}
+
 __global__ void __launch_bounds__(128)
 galerkin_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ KF,
-                double* __restrict__ KC, int zident) {
+                double* __restrict__ KC, int zident, int fast) {
     const int I = blockIdx.x * 128 + threadIdx.x;
     const int J = blockIdx.y, Kc = blockIdx.z;
     if (I < 1 || I > C.n1 - 2 || !row_free(C, J) || Kc > C.n3 - 2) return;
-    if (zident && regular1d(M.pos[0], C.n1, I) && regular1d(M.pos[1], C.n2, J)) {
+    const bool xyreg = fast && regular1d(M.pos[0], C.n1, I) && regular1d(M.pos[1], C.n2, J);
+    if (xyreg && !zident) {
+        const int fi = M.pos[0][I], fj = M.pos[1][J];
+        int t0[9], d0[9], t1[9], d1[9];
+        double w0[9], w1[9];
+        const int n0 = zpairs(M, F.n3, Kc, 0, t0, d0, w0);
+        const int n1 = zpairs(M, F.n3, Kc, 1, t1, d1, w1);
+        double* o = KC + loff(C, I, J, Kc);
+        o[0 * C.NT] = galerkin_xyreg<0, 0>(F, KF, fi, fj, t0, d0, w0, n0);
+        o[1 * C.NT] = galerkin_xyreg<1, 0>(F, KF, fi, fj, t0, d0, w0, n0);
+        o[2 * C.NT] = galerkin_xyreg<-1, 1>(F, KF, fi, fj, t0, d0, w0, n0);
+        o[3 * C.NT] = galerkin_xyreg<0, 1>(F, KF, fi, fj, t0, d0, w0, n0);
+        o[4 * C.NT] = galerkin_xyreg<1, 1>(F, KF, fi, fj, t0, d0, w0, n0);
+        o[5 * C.NT] = galerkin_xyreg<-1, -1>(F, KF, fi, fj, t1, d1, w1, n1);
+        o[6 * C.NT] = galerkin_xyreg<0, -1>(F, KF, fi, fj, t1, d1, w1, n1);
+        o[7 * C.NT] = galerkin_xyreg<1, -1>(F, KF, fi, fj, t1, d1, w1, n1);
+        o[8 * C.NT] = galerkin_xyreg<-1, 0>(F, KF, fi, fj, t1, d1, w1, n1);
+        o[9 * C.NT] = galerkin_xyreg<0, 0>(F, KF, fi, fj, t1, d1, w1, n1);
+        o[10 * C.NT] = galerkin_xyreg<1, 0>(F, KF, fi, fj, t1, d1, w1, n1);
+        o[11 * C.NT] = galerkin_xyreg<-1, 1>(F, KF, fi, fj, t1, d1, w1, n1);
+        o[12 * C.NT] = galerkin_xyreg<0, 1>(F, KF, fi, fj, t1, d1, w1, n1);
+        o[13 * C.NT] = galerkin_xyreg<1, 1>(F, KF, fi, fj, t1, d1, w1, n1);
+        return;
+    }
+    if (xyreg) {   // identity z
         const int fi = M.pos[0][I], fj = M.pos[1][J];
         const i64 out = loff(C, I, J, Kc);
         double* o = KC + out;
@@ -702,7 +774,7 @@ void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const d
                      double* coefC, int zident, cudaStream_t st) {
     dim3 grid((Cl.n1 + 127) / 128, Cl.n2, Cl.n3);
     g_launches += 1;
-    galerkin_kernel<<<grid, 128, 0, st>>>(F, Cl, M, coefF, coefC, zident && !g_galerkin_generic);
+    galerkin_kernel<<<grid, 128, 0, st>>>(F, Cl, M, coefF, coefC, zident, !g_galerkin_generic);
 }
 
 void launch_export27(const LevDev& L, const double* coef, double* K27, cudaStream_t st) {

@@ -173,12 +173,21 @@ def test_fused_sweep_matches_oracle_small(wd):
     ctx.close()
 
 
-@pytest.mark.parametrize("name", ["small", "ragged_a", "ragged_b"])
+ZMERGE = {
+    # fine vertical spacing against the horizontal one: the planner merges
+    # layers after the first horizontal coarsenings (non-identity z maps)
+    "zmerge": lambda: synth.hill(nx=120, ny=97, nz=12, dx=15.0, height=60.0, sigma=400.0,
+                                 dz0=3.0, r=1.3, a=(1, 1, 1)),
+}
+
+
+@pytest.mark.parametrize("name", ["small", "ragged_a", "ragged_b", "zmerge"])
 def test_galerkin_unrolled_path_bitwise(wd, name, monkeypatch):
-    """The unrolled Galerkin path (regular interior columns, identity z map)
-    performs the generic kernel's products and sums in the same order: the
-    coarse operators must be bit-for-bit those of the generic path."""
-    p = GRIDS[name]()
+    """The unrolled Galerkin paths (regular interior columns; identity z map,
+    or layers merged with the z pairs built at run time) perform the generic
+    kernel's products and sums in the same order: the coarse operators must
+    be bit-for-bit those of the generic path."""
+    p = (GRIDS.get(name) or ZMERGE[name])()
     g = p.to(DEV)
     opt = wd.default_options(coarsest_max_free=60)
     fast = wd.wd_assemble(g.X, g.Y, g.Z, p.a, opt)
@@ -186,6 +195,9 @@ def test_galerkin_unrolled_path_bitwise(wd, name, monkeypatch):
     gen = wd.wd_assemble(g.X, g.Y, g.Z, p.a, opt)
     monkeypatch.delenv("WD_GALERKIN_GENERIC")
     assert fast.num_levels() == gen.num_levels()
+    if name in ZMERGE:
+        n3s = [fast.level_dims(l)[2] for l in range(fast.num_levels())]
+        assert any(b < a for a, b in zip(n3s, n3s[1:])), n3s
     for l in range(1, fast.num_levels()):
         a = wd.wd_get_stencil(fast, l)
         b = wd.wd_get_stencil(gen, l)
