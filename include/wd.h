@@ -149,6 +149,12 @@ int wd_vcycle(wd_ctx* ctx, double* lambda, const double* f, double* rel_res_out,
  * until ||f - K lambda||/||f|| <= rel_tol (in (0,1)), max_cycles, divergence
  * or a non-finite residual.  f = 0 returns lambda = 0 after 0 cycles.
  * lambda (out) may alias lambda0.  rep (nullable, host) is filled.
+ * The test is made after every cycle.  With the fused smoother (and at least
+ * one pre-smoothing sweep on a multi-level hierarchy) the residual of iterate
+ * c is returned by the first sweep of cycle c+1, which reads that iterate
+ * unchanged; if the test passes the sweep's output is discarded, so the
+ * result and the cycle count are those of "cycle, then test" (the residual
+ * agrees with a separate residual pass to rounding, about 1e-13 of ||f||).
  * Returns WD_OK, WD_E_NOCONV, WD_E_DIVERGED or WD_E_NONFINITE (lambda is the
  * last iterate in every case). */
 int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol,
