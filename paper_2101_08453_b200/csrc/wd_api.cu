@@ -811,13 +811,24 @@ int run_split(wd_ctx* ctx, int which, cudaStream_t st) {
             if (which == 2) return fail(WD_E_INVAL, "split V-cycle: rest before first sweep");
             // capture all three from the canonical state: the two first-sweep
             // variants each swap the level-0 buffers, the rest swaps them back
-            RC(capture_graph(ctx, &ctx->g_first, &ctx->k_first,
-                             [&](cudaStream_t s) { return smooth(ctx, 0, prof, 0, s); }));
+            cudaGraphExec_t g1 = nullptr, g0 = nullptr, g2 = nullptr;
+            long long k1 = 0, k0 = 0, k2 = 0;
+            int rc = capture_graph(ctx, &g1, &k1,
+                                   [&](cudaStream_t s) { return smooth(ctx, 0, prof, 0, s); });
             for (Part& P : ctx->parts) std::swap(P.lev[0].lam, P.lev[0].lam2);
-            RC(capture_graph(ctx, &ctx->g_first_res, &ctx->k_first_res,
-                             [&](cudaStream_t s) { return smooth_first_res(ctx, prof, s); }));
-            RC(capture_graph(ctx, &ctx->g_rest, &ctx->k_rest,
-                             [&](cudaStream_t s) { return vcycle_level(ctx, 0, s, 1); }));
+            if (!rc)
+                rc = capture_graph(ctx, &g0, &k0,
+                                   [&](cudaStream_t s) { return smooth_first_res(ctx, prof, s); });
+            if (!rc)
+                rc = capture_graph(ctx, &g2, &k2,
+                                   [&](cudaStream_t s) { return vcycle_level(ctx, 0, s, 1); });
+            if (rc) {
+                for (cudaGraphExec_t g : {g1, g0, g2})
+                    if (g) cudaGraphExecDestroy(g);
+                return rc;
+            }
+            ctx->g_first = g1, ctx->g_first_res = g0, ctx->g_rest = g2;
+            ctx->k_first = k1, ctx->k_first_res = k0, ctx->k_rest = k2;
             // host roles now canonical; replay the first sweep's swap below
         }
         cudaGraphExec_t g = which == 0 ? ctx->g_first_res : which == 1 ? ctx->g_first : ctx->g_rest;
