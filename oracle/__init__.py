@@ -83,6 +83,12 @@ def num_threads() -> int:
     return int(lib().orc_num_threads())
 
 
+def set_threads(n: int) -> None:
+    """Thread count of the oracle's OpenMP regions (the result does not depend
+    on it: the scatter loops are owner-partitioned, see orc.c own_rows)."""
+    lib().orc_set_threads(int(n))
+
+
 def _d(a):
     assert a.dtype == np.float64 and a.flags.c_contiguous, (a.dtype, a.flags)
     return a.ctypes.data_as(_dp)

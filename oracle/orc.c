@@ -60,6 +60,31 @@ int orc_num_threads(void) {
 #endif
 }
 
+/* Thread count of the parallel regions (tests compare 1 thread with many). */
+void orc_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
+/* Owner partition of the scatter loops (element assembly, RHS, Galerkin,
+ * restriction): inside a parallel region, thread t owns the target rows
+ * [*r0, *r1) of n.  Each thread runs the SERIAL loop in its serial order and
+ * adds only into the rows it owns, so every target entry receives the same
+ * terms in the same order as in the one-thread loop: the result is bitwise
+ * that of the serial code (tests/test_oracle_threads.py checks it). */
+static void own_rows(int n, int* r0, int* r1) {
+#ifdef _OPENMP
+    const int t = omp_get_thread_num(), T = omp_get_num_threads();
+#else
+    const int t = 0, T = 1;
+#endif
+    *r0 = (int)((i64)n * t / T);
+    *r1 = (int)((i64)n * (t + 1) / T);
+}
+
 /* ------------------------------------------------------------------ */
 /* isoparametric trilinear hexahedron                       */
 /* ------------------------------------------------------------------ */
@@ -337,22 +362,30 @@ int orc_assemble(const double* X, const double* Y, const double* Z, int n1, int 
                  const double c[3], double* K) {
     i64 N = (i64)n1 * n2 * n3;
     memset(K, 0, sizeof(double) * 27 * N);
-    double xe[24], Ke[64];
-    for (int k = 0; k < n3 - 1; k++)
-        for (int j = 0; j < n2 - 1; j++)
-            for (int i = 0; i < n1 - 1; i++) {
-                gather_xe(X, Y, Z, n1, n2, i, j, k, xe);
-                if (orc_element_stiffness(xe, c, Ke) < 0) return -1;
-                for (int a = 0; a < 8; a++) {
-                    i64 p = enode(n1, n2, i, j, k, a);
-                    for (int b = 0; b < 8; b++) {
-                        int o = o27(((b & 1) - (a & 1)), (((b >> 1) & 1) - ((a >> 1) & 1)),
-                                    (((b >> 2) & 1) - ((a >> 2) & 1)));
-                        K[p * 27 + o] += Ke[a * 8 + b];
+    int bad = 0;
+#pragma omp parallel reduction(| : bad)
+    {
+        int J0, J1;
+        own_rows(n2, &J0, &J1);   /* node rows owned by this thread */
+        double xe[24], Ke[64];
+        for (int k = 0; k < n3 - 1 && !bad; k++)
+            for (int j = (J0 > 0 ? J0 - 1 : 0); j < n2 - 1 && j < J1; j++)
+                for (int i = 0; i < n1 - 1; i++) {
+                    gather_xe(X, Y, Z, n1, n2, i, j, k, xe);
+                    if (orc_element_stiffness(xe, c, Ke) < 0) { bad = 1; break; }
+                    for (int a = 0; a < 8; a++) {
+                        const int ja = j + ((a >> 1) & 1);
+                        if (ja < J0 || ja >= J1) continue;
+                        i64 p = enode(n1, n2, i, j, k, a);
+                        for (int b = 0; b < 8; b++) {
+                            int o = o27(((b & 1) - (a & 1)), (((b >> 1) & 1) - ((a >> 1) & 1)),
+                                        (((b >> 2) & 1) - ((a >> 2) & 1)));
+                            K[p * 27 + o] += Ke[a * 8 + b];
+                        }
                     }
                 }
-            }
-    return 0;
+    }
+    return bad ? -1 : 0;
 }
 
 /* One-point stiffness K1 (C12 identity only). */
@@ -360,22 +393,30 @@ int orc_assemble_onepoint(const double* X, const double* Y, const double* Z, int
                           int n3, const double c[3], double* K) {
     i64 N = (i64)n1 * n2 * n3;
     memset(K, 0, sizeof(double) * 27 * N);
-    double xe[24], Ke[64];
-    for (int k = 0; k < n3 - 1; k++)
-        for (int j = 0; j < n2 - 1; j++)
-            for (int i = 0; i < n1 - 1; i++) {
-                gather_xe(X, Y, Z, n1, n2, i, j, k, xe);
-                if (orc_element_stiffness_onepoint(xe, c, Ke) < 0) return -1;
-                for (int a = 0; a < 8; a++) {
-                    i64 p = enode(n1, n2, i, j, k, a);
-                    for (int b = 0; b < 8; b++) {
-                        int o = o27(((b & 1) - (a & 1)), (((b >> 1) & 1) - ((a >> 1) & 1)),
-                                    (((b >> 2) & 1) - ((a >> 2) & 1)));
-                        K[p * 27 + o] += Ke[a * 8 + b];
+    int bad = 0;
+#pragma omp parallel reduction(| : bad)
+    {
+        int J0, J1;
+        own_rows(n2, &J0, &J1);   /* node rows owned by this thread */
+        double xe[24], Ke[64];
+        for (int k = 0; k < n3 - 1 && !bad; k++)
+            for (int j = (J0 > 0 ? J0 - 1 : 0); j < n2 - 1 && j < J1; j++)
+                for (int i = 0; i < n1 - 1; i++) {
+                    gather_xe(X, Y, Z, n1, n2, i, j, k, xe);
+                    if (orc_element_stiffness_onepoint(xe, c, Ke) < 0) { bad = 1; break; }
+                    for (int a = 0; a < 8; a++) {
+                        const int ja = j + ((a >> 1) & 1);
+                        if (ja < J0 || ja >= J1) continue;
+                        i64 p = enode(n1, n2, i, j, k, a);
+                        for (int b = 0; b < 8; b++) {
+                            int o = o27(((b & 1) - (a & 1)), (((b >> 1) & 1) - ((a >> 1) & 1)),
+                                        (((b >> 2) & 1) - ((a >> 2) & 1)));
+                            K[p * 27 + o] += Ke[a * 8 + b];
+                        }
                     }
                 }
-            }
-    return 0;
+    }
+    return bad ? -1 : 0;
 }
 
 /* RHS f = sum_e fe (element loop, natural order); f_D = 0.
@@ -385,18 +426,28 @@ int orc_rhs(const double* X, const double* Y, const double* Z, int n1, int n2, i
     int nx = n1 - 1, ny = n2 - 1, nz = n3 - 1;
     i64 N = (i64)n1 * n2 * n3, E = (i64)nx * ny * nz;
     memset(f, 0, sizeof(double) * N);
-    double xe[24], fe[8], ue[3];
-    for (int k = 0; k < nz; k++)
-        for (int j = 0; j < ny; j++)
-            for (int i = 0; i < nx; i++) {
-                i64 e = ((i64)k * ny + j) * nx + i;
-                gather_xe(X, Y, Z, n1, n2, i, j, k, xe);
-                ue[0] = u0[e];
-                ue[1] = u0[E + e];
-                ue[2] = u0[2 * E + e];
-                if (orc_element_rhs(xe, ue, fe) < 0) return -1;
-                for (int a = 0; a < 8; a++) f[enode(n1, n2, i, j, k, a)] += fe[a];
-            }
+    int bad = 0;
+#pragma omp parallel reduction(| : bad)
+    {
+        int J0, J1;
+        own_rows(n2, &J0, &J1);   /* node rows owned by this thread */
+        double xe[24], fe[8], ue[3];
+        for (int k = 0; k < nz && !bad; k++)
+            for (int j = (J0 > 0 ? J0 - 1 : 0); j < ny && j < J1; j++)
+                for (int i = 0; i < nx; i++) {
+                    i64 e = ((i64)k * ny + j) * nx + i;
+                    gather_xe(X, Y, Z, n1, n2, i, j, k, xe);
+                    ue[0] = u0[e];
+                    ue[1] = u0[E + e];
+                    ue[2] = u0[2 * E + e];
+                    if (orc_element_rhs(xe, ue, fe) < 0) { bad = 1; break; }
+                    for (int a = 0; a < 8; a++) {
+                        const int ja = j + ((a >> 1) & 1);
+                        if (ja >= J0 && ja < J1) f[enode(n1, n2, i, j, k, a)] += fe[a];
+                    }
+                }
+    }
+    if (bad) return -1;
     for (int k = 0; k < n3; k++)
         for (int j = 0; j < n2; j++)
             for (int i = 0; i < n1; i++)
@@ -411,20 +462,28 @@ int orc_d1(const double* X, const double* Y, const double* Z, int n1, int n2, in
     int nx = n1 - 1, ny = n2 - 1, nz = n3 - 1;
     i64 N = (i64)n1 * n2 * n3, E = (i64)nx * ny * nz;
     memset(out, 0, sizeof(double) * N);
-    double xe[24], G[24], B[24];
+    double G[24];
     const double xi[3] = {0.0, 0.0, 0.0};
     orc_shape_grad(xi, G);
-    for (int k = 0; k < nz; k++)
-        for (int j = 0; j < ny; j++)
-            for (int i = 0; i < nx; i++) {
-                i64 e = ((i64)k * ny + j) * nx + i;
-                gather_xe(X, Y, Z, n1, n2, i, j, k, xe);
-                double det = phys_grad(xe, G, B);
-                for (int a = 0; a < 8; a++) {
-                    double s = B[a * 3 + 0] * v[e] + B[a * 3 + 1] * v[E + e] + B[a * 3 + 2] * v[2 * E + e];
-                    out[enode(n1, n2, i, j, k, a)] += 8.0 * det * s;
+#pragma omp parallel
+    {
+        int J0, J1;
+        own_rows(n2, &J0, &J1);   /* node rows owned by this thread */
+        double xe[24], B[24];
+        for (int k = 0; k < nz; k++)
+            for (int j = (J0 > 0 ? J0 - 1 : 0); j < ny && j < J1; j++)
+                for (int i = 0; i < nx; i++) {
+                    i64 e = ((i64)k * ny + j) * nx + i;
+                    gather_xe(X, Y, Z, n1, n2, i, j, k, xe);
+                    double det = phys_grad(xe, G, B);
+                    for (int a = 0; a < 8; a++) {
+                        const int ja = j + ((a >> 1) & 1);
+                        if (ja < J0 || ja >= J1) continue;
+                        double s = B[a * 3 + 0] * v[e] + B[a * 3 + 1] * v[E + e] + B[a * 3 + 2] * v[2 * E + e];
+                        out[enode(n1, n2, i, j, k, a)] += 8.0 * det * s;
+                    }
                 }
-            }
+    }
     for (int k = 0; k < n3; k++)
         for (int j = 0; j < n2; j++)
             for (int i = 0; i < n1; i++)
@@ -731,9 +790,21 @@ static int galerkin(const orc_level* f, orc_level* c) {
     int n1 = f->n1, n2 = f->n2, n3 = f->n3;
     int m1 = c->n1, m2 = c->n2, m3 = c->n3;
     memset(c->K, 0, sizeof(double) * 27 * level_N(c));
-    for (int k = 0; k < n3 - 1; k++)
-        for (int j = 1; j < n2 - 1; j++)
-            for (int i = 1; i < n1 - 1; i++) {
+    int bad = 0;
+#pragma omp parallel reduction(| : bad)
+    {
+    int C0, C1;
+    own_rows(m2, &C0, &C1);   /* coarse rows owned by this thread */
+    for (int k = 0; k < n3 - 1 && !bad; k++)
+        for (int j = 1; j < n2 - 1 && !bad; j++) {
+            {   /* skip fine rows with no parent row owned here */
+                int pj[2];
+                double wj[2];
+                int np = parents(f, 1, j, pj, wj), any = 0;
+                for (int t = 0; t < np; t++) any |= pj[t] >= C0 && pj[t] < C1;
+                if (!any) continue;
+            }
+            for (int i = 1; i < n1 - 1 && !bad; i++) {
                 i64 p = nid(n1, n2, i, j, k);
                 int pci[2], pcj[2], pck[2];
                 double pwi[2], pwj[2], pwk[2];
@@ -755,6 +826,7 @@ static int galerkin(const orc_level* f, orc_level* c) {
                                 for (int a2 = 0; a2 < npj; a2++)
                                     for (int a1 = 0; a1 < npi; a1++) {
                                         int Pi = pci[a1], Pj = pcj[a2], Pk = pck[a3];
+                                        if (Pj < C0 || Pj >= C1) continue;
                                         if (is_dir(m1, m2, m3, Pi, Pj, Pk)) continue;
                                         double wP = pwi[a1] * pwj[a2] * pwk[a3];
                                         i64 P = nid(m1, m2, Pi, Pj, Pk);
@@ -762,15 +834,19 @@ static int galerkin(const orc_level* f, orc_level* c) {
                                             for (int b2 = 0; b2 < nqj; b2++)
                                                 for (int b1 = 0; b1 < nqi; b1++) {
                                                     int ex = qci[b1] - Pi, ey = qcj[b2] - Pj, ez = qck[b3] - Pk;
-                                                    if (ex < -1 || ex > 1 || ey < -1 || ey > 1 || ez < -1 || ez > 1)
-                                                        return -1;
+                                                    if (ex < -1 || ex > 1 || ey < -1 || ey > 1 || ez < -1 || ez > 1) {
+                                                        bad = 1;
+                                                        continue;
+                                                    }
                                                     double wQ = qwi[b1] * qwj[b2] * qwk[b3];
                                                     c->K[P * 27 + o27(ex, ey, ez)] += wP * kpq * wQ;
                                                 }
                                     }
                         }
             }
-    return 0;
+        }
+    }
+    return bad ? -1 : 0;
 }
 
 /* f_c = P^T r (Eq. (7) "f_c = P^T (f - K u)"), scatter over fine free p into
@@ -778,8 +854,19 @@ static int galerkin(const orc_level* f, orc_level* c) {
 static void restrict_(const orc_level* f, const orc_level* c, const double* r, double* fc) {
     int n1 = f->n1, n2 = f->n2, n3 = f->n3;
     memset(fc, 0, sizeof(double) * level_N(c));
+#pragma omp parallel
+    {
+    int C0, C1;
+    own_rows(c->n2, &C0, &C1);   /* coarse rows owned by this thread */
     for (int k = 0; k < n3 - 1; k++)
-        for (int j = 1; j < n2 - 1; j++)
+        for (int j = 1; j < n2 - 1; j++) {
+            {   /* skip fine rows with no parent row owned here */
+                int pj[2];
+                double wj[2];
+                int np = parents(f, 1, j, pj, wj), any = 0;
+                for (int t = 0; t < np; t++) any |= pj[t] >= C0 && pj[t] < C1;
+                if (!any) continue;
+            }
             for (int i = 1; i < n1 - 1; i++) {
                 double rp = r[nid(n1, n2, i, j, k)];
                 int pci[2], pcj[2], pck[2];
@@ -790,11 +877,14 @@ static void restrict_(const orc_level* f, const orc_level* c, const double* r, d
                 for (int a3 = 0; a3 < npk; a3++)
                     for (int a2 = 0; a2 < npj; a2++)
                         for (int a1 = 0; a1 < npi; a1++) {
+                            if (pcj[a2] < C0 || pcj[a2] >= C1) continue;
                             if (is_dir(c->n1, c->n2, c->n3, pci[a1], pcj[a2], pck[a3])) continue;
                             fc[nid(c->n1, c->n2, pci[a1], pcj[a2], pck[a3])] +=
                                 pwi[a1] * pwj[a2] * pwk[a3] * rp;
                         }
             }
+        }
+    }
 }
 
 /* x += P x_c (Eq. (7) "u <- u + P u_c") on fine free nodes; x_c,D = 0. */
