@@ -249,6 +249,18 @@ def gs_sweep(K, x, f):
     return x
 
 
+def planner_inputs(X, Y, Z):
+    """(h1, h3) the planner starts from (orc_planner_inputs, reading C2):
+    h1 = sqrt(dx dy) at the grid origin, h3 = the layer thicknesses of the
+    column of minimum Z(i,j,0), ties -> smallest linear index."""
+    n3, n2, n1 = X.shape
+    h1 = C.c_double(0)
+    h3 = np.zeros(n3 - 1)
+    lib().orc_planner_inputs(_d(_f64(X)), _d(_f64(Y)), _d(_f64(Z)), n1, n2, n3, C.byref(h1),
+                             _d(h3))
+    return h1.value, h3
+
+
 def plan_level(h1, h3, a, rule="coupling_cur", n1=1001, n2=1001):
     h3 = _f64(h3)
     nz = len(h3)

@@ -134,9 +134,23 @@ def _check(rc, ok=(WD_OK,)):
 
 
 def _ptr(t: torch.Tensor):
-    assert t.dtype == torch.float64, t.dtype
-    assert t.is_contiguous()
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_contiguous():
+        raise WDError(WD_E_INVAL, "arguments must be contiguous float64 tensors "
+                      f"(got {getattr(t, 'dtype', type(t))})")
     return C.c_void_p(t.data_ptr())
+
+
+def _arg(ctx: "Context", t: torch.Tensor, shape, name: str):
+    """Validate a tensor crossing the ABI against the context: the C side takes
+    every size from the context, so a wrong shape or another GPU's tensor would
+    read or write out of bounds.  Host tensors are allowed (staged inside)."""
+    if not isinstance(t, torch.Tensor):
+        raise WDError(WD_E_INVAL, f"{name}: expected a torch.Tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise WDError(WD_E_INVAL, f"{name}: shape {tuple(t.shape)} != expected {tuple(shape)}")
+    if t.is_cuda and t.device != ctx.device:
+        raise WDError(WD_E_INVAL, f"{name}: on {t.device}, context on {ctx.device}")
+    return _ptr(t)
 
 
 def _stream(t: torch.Tensor):
@@ -275,6 +289,9 @@ def wd_assemble(X, Y, Z, a, opt: wd_options | None = None, n2_global=None) -> Co
     """X, Y, Z: node arrays (n3, rows, n1); rows = n2 except in NCCL mode, where
     they hold this rank's slab (slab_rows) and n2_global gives the grid's n2."""
     n3, rows, n1 = X.shape
+    for name, t in (("Y", Y), ("Z", Z)):
+        if tuple(t.shape) != tuple(X.shape) or t.device != X.device:
+            raise WDError(WD_E_INVAL, f"{name}: shape/device differ from X")
     n2 = int(n2_global) if n2_global is not None else rows
     h = C.c_void_p()
     o = opt if opt is not None else default_options()
@@ -286,14 +303,16 @@ def wd_assemble(X, Y, Z, a, opt: wd_options | None = None, n2_global=None) -> Co
 def wd_rhs(ctx: Context, u0, f=None):
     if f is None:
         f = torch.empty(ctx.node_shape, dtype=torch.float64, device=u0.device)
-    _check(_lib.wd_rhs(ctx.h, _ptr(u0), _ptr(f), _stream(u0)))
+    _check(_lib.wd_rhs(ctx.h, _arg(ctx, u0, ctx.elem_shape, "u0"),
+                       _arg(ctx, f, ctx.node_shape, "f"), _stream(u0)))
     return f
 
 
 def wd_vcycle(ctx: Context, lam, f, want_residual=True):
     rel = C.c_double(0)
-    _check(_lib.wd_vcycle(ctx.h, _ptr(lam), _ptr(f), C.byref(rel) if want_residual else None,
-                          _stream(lam)))
+    _check(_lib.wd_vcycle(ctx.h, _arg(ctx, lam, ctx.node_shape, "lam"),
+                          _arg(ctx, f, ctx.node_shape, "f"),
+                          C.byref(rel) if want_residual else None, _stream(lam)))
     return rel.value if want_residual else None
 
 
@@ -301,8 +320,10 @@ def wd_solve(ctx: Context, f, lam0=None, rel_tol=1e-8, lam=None, raise_on_noconv
     if lam is None:
         lam = torch.empty(ctx.node_shape, dtype=torch.float64, device=f.device)
     rep = wd_report()
-    rc = _lib.wd_solve(ctx.h, _ptr(f), None if lam0 is None else _ptr(lam0), float(rel_tol),
-                       _ptr(lam), C.byref(rep), _stream(f))
+    rc = _lib.wd_solve(ctx.h, _arg(ctx, f, ctx.node_shape, "f"),
+                       None if lam0 is None else _arg(ctx, lam0, ctx.node_shape, "lam0"),
+                       float(rel_tol), _arg(ctx, lam, ctx.node_shape, "lam"), C.byref(rep),
+                       _stream(f))
     ok = (WD_OK,) if raise_on_noconv else (WD_OK, WD_E_NOCONV, WD_E_DIVERGED, WD_E_NONFINITE)
     _check(rc, ok)
     return lam, rep.to_dict()
@@ -311,7 +332,9 @@ def wd_solve(ctx: Context, f, lam0=None, rel_tol=1e-8, lam=None, raise_on_noconv
 def wd_recover_wind(ctx: Context, lam, u0, u=None):
     if u is None:
         u = torch.empty_like(u0)
-    _check(_lib.wd_recover_wind(ctx.h, _ptr(lam), _ptr(u0), _ptr(u), _stream(u0)))
+    _check(_lib.wd_recover_wind(ctx.h, _arg(ctx, lam, ctx.node_shape, "lam"),
+                                _arg(ctx, u0, ctx.elem_shape, "u0"),
+                                _arg(ctx, u, ctx.elem_shape, "u"), _stream(u0)))
     return u
 
 
@@ -319,43 +342,51 @@ def wd_recover_wind(ctx: Context, lam, u0, u=None):
 def wd_get_stencil(ctx: Context, level=0, device=None):
     n3, n2, n1 = ctx.level_shape(level)
     K = torch.empty((n3, n2, n1, 27), dtype=torch.float64, device=device or ctx.device)
-    _check(_lib.wd_get_stencil(ctx.h, level, _ptr(K), _stream(K)))
+    _check(_lib.wd_get_stencil(ctx.h, level, _arg(ctx, K, (n3, n2, n1, 27), "K"), _stream(K)))
     return K
 
 
 def wd_apply(ctx: Context, level, x, y=None):
     y = torch.empty_like(x) if y is None else y
-    _check(_lib.wd_apply(ctx.h, level, _ptr(x), _ptr(y), _stream(x)))
+    sh = ctx.level_shape(level)
+    _check(_lib.wd_apply(ctx.h, level, _arg(ctx, x, sh, "x"), _arg(ctx, y, sh, "y"), _stream(x)))
     return y
 
 
 def wd_smooth(ctx: Context, level, x, f, sweeps=1):
-    _check(_lib.wd_smooth(ctx.h, level, _ptr(x), _ptr(f), int(sweeps), _stream(x)))
+    sh = ctx.level_shape(level)
+    _check(_lib.wd_smooth(ctx.h, level, _arg(ctx, x, sh, "x"), _arg(ctx, f, sh, "f"),
+                          int(sweeps), _stream(x)))
     return x
 
 
 def wd_restrict(ctx: Context, level, r, fc=None):
     if fc is None:
         fc = torch.empty(ctx.level_shape(level + 1), dtype=torch.float64, device=r.device)
-    _check(_lib.wd_restrict(ctx.h, level, _ptr(r), _ptr(fc), _stream(r)))
+    _check(_lib.wd_restrict(ctx.h, level, _arg(ctx, r, ctx.level_shape(level), "r"),
+                            _arg(ctx, fc, ctx.level_shape(level + 1), "fc"), _stream(r)))
     return fc
 
 
 def wd_prolong(ctx: Context, level, xc, x):
-    _check(_lib.wd_prolong(ctx.h, level, _ptr(xc), _ptr(x), _stream(x)))
+    _check(_lib.wd_prolong(ctx.h, level, _arg(ctx, xc, ctx.level_shape(level + 1), "xc"),
+                           _arg(ctx, x, ctx.level_shape(level), "x"), _stream(x)))
     return x
 
 
 def wd_coarse_solve(ctx: Context, f, x=None):
     x = torch.empty_like(f) if x is None else x
-    _check(_lib.wd_coarse_solve(ctx.h, _ptr(f), _ptr(x), _stream(f)))
+    sh = ctx.level_shape(ctx.num_levels() - 1)
+    _check(_lib.wd_coarse_solve(ctx.h, _arg(ctx, f, sh, "f"), _arg(ctx, x, sh, "x"), _stream(f)))
     return x
 
 
 def wd_residual_norm(ctx: Context, x, f):
     a = C.c_double()
     r = C.c_double()
-    _check(_lib.wd_residual_norm(ctx.h, _ptr(x), _ptr(f), C.byref(a), C.byref(r), _stream(x)))
+    _check(_lib.wd_residual_norm(ctx.h, _arg(ctx, x, ctx.node_shape, "x"),
+                                 _arg(ctx, f, ctx.node_shape, "f"), C.byref(a), C.byref(r),
+                                 _stream(x)))
     return a.value, r.value
 
 
@@ -399,6 +430,9 @@ def wd_interp_wind(uc: torch.Tensor, xc0, yc0, DXc, DYc, hc, X, Y, Z):
     h = _host_f64(hc)
     _, nzc, nyc, nxc = uc.shape
     n3, n2, n1 = X.shape
+    for name, t in (("Y", Y), ("Z", Z)):
+        if tuple(t.shape) != tuple(X.shape) or t.device != X.device:
+            raise WDError(WD_E_INVAL, f"{name}: shape/device differ from X")
     u0 = torch.empty((3, n3 - 1, n2 - 1, n1 - 1), dtype=torch.float64, device=X.device)
     _check(_lib.wd_interp_wind(_ptr(uc), nxc, nyc, nzc, float(xc0), float(yc0), float(DXc),
                                float(DYc), h.ctypes.data_as(C.c_void_p), _ptr(X), _ptr(Y), _ptr(Z),
@@ -409,7 +443,7 @@ def wd_interp_wind(uc: torch.Tensor, xc0, yc0, DXc, DYc, hc, X, Y, Z):
 def wd_mass_consistency(ctx: Context, u):
     """(l2, max) of the one-point weak divergence D1(u) over free nodes."""
     out = (C.c_double * 2)()
-    _check(_lib.wd_mass_consistency(ctx.h, _ptr(u), out, _stream(u)))
+    _check(_lib.wd_mass_consistency(ctx.h, _arg(ctx, u, ctx.elem_shape, "u"), out, _stream(u)))
     return float(out[0]), float(out[1])
 
 
@@ -420,8 +454,10 @@ def wd_downscale_step(ctx: Context, u0, lam, warm=True, rel_tol=1e-8, u=None,
     if u is None:
         u = torch.empty_like(u0)
     rep = wd_report()
-    rc = _lib.wd_downscale_step(ctx.h, _ptr(u0), _ptr(lam), 1 if warm else 0, float(rel_tol),
-                                _ptr(u), C.byref(rep), _stream(u0))
+    rc = _lib.wd_downscale_step(ctx.h, _arg(ctx, u0, ctx.elem_shape, "u0"),
+                                _arg(ctx, lam, ctx.node_shape, "lam"), 1 if warm else 0,
+                                float(rel_tol), _arg(ctx, u, ctx.elem_shape, "u"), C.byref(rep),
+                                _stream(u0))
     ok = (WD_OK,) if raise_on_noconv else (WD_OK, WD_E_NOCONV, WD_E_DIVERGED, WD_E_NONFINITE)
     _check(rc, ok)
     return u, rep.to_dict()

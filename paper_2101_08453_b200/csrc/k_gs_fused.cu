@@ -52,6 +52,7 @@
 #include "wd_internal.cuh"
 
 #include <algorithm>
+#include <atomic>
 
 namespace wd {
 
@@ -342,21 +343,32 @@ gs_fused_kernel(LevDev L, const double* __restrict__ K, const double* __restrict
 
 }  // namespace
 
+// Per-device setup (the dynamic shared-memory limit is a per-device function
+// attribute): done once per device, from wd_assemble and on first use; the
+// SM count is cached per device.  Setting an attribute twice is harmless, so
+// concurrent first calls need no lock.
+int gs_fused_prepare() {
+    static std::atomic<int> nsm_dev[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int nsm = nsm_dev[dev].load(std::memory_order_acquire);
+    if (nsm > 0) return nsm;
+    cudaFuncSetAttribute(gs_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(gs_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RES);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+    nsm_dev[dev].store(nsm, std::memory_order_release);
+    return nsm;
+}
+
 // one sweep: lin (old iterate, unchanged) -> lout (new iterate on the owned
 // free nodes; D entries of lout must already be 0).  partial != NULL: also
 // ||f - K lin||^2 over the owned free nodes as one partial per CTA; returns
 // the number of CTAs (partials)
 int launch_gs_fused(const LevDev& L, const double* coef, const double* lin, double* lout,
                     const double* f, cudaStream_t st, double* partial) {
-    static int nsm = 0;
-    if (!nsm) {
-        cudaFuncSetAttribute(gs_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        cudaFuncSetAttribute(gs_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RES);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (nsm <= 0) nsm = 148;
-    }
+    const int nsm = gs_fused_prepare();
     // tiles of TJ rows from the even global row at or below the first owned row
     const int jt0 = L.own0 - ((L.own0 + L.jg0) & 1);
     const int ntx = (L.n1 + TI - 1) / TI, nty = (L.own1 - jt0 + TJ - 1) / TJ;

@@ -381,7 +381,7 @@ restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
 
 __global__ void __launch_bounds__(128)
 prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
-               double* __restrict__ x, int zident) {
+               double* __restrict__ x, int zident, double w) {
     const int i = blockIdx.x * 128 + threadIdx.x;
     const int j = blockIdx.y;
     if (i < 1 || i > F.n1 - 2 || !row_free(F, j)) return;
@@ -409,7 +409,9 @@ prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
                 sr2 += two ? ldg(c3 + kc) : -0.0;
                 s = fma(wy * 1.0, wx * sr2, s);
             }
-            xo[(i64)k * F.sk] += s;
+            // x + w s: with w = 1 (Eq. (7)) the product is exact, so this is
+            // x + s bit for bit; w != 1 only for the divergence-guard test
+            xo[(i64)k * F.sk] = fma(w, s, xo[(i64)k * F.sk]);
         }
         return;
     }
@@ -426,7 +428,7 @@ prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
                 s = fma(wy * wz, wx * sr, s);
             }
         const i64 o = loff(F, i, j, k);
-        x[o] += s;
+        x[o] = fma(w, s, x[o]);
     }
 }
 
@@ -764,10 +766,10 @@ void launch_restrict(const LevDev& F, const LevDev& Cl, const MapDev& M, const d
 }
 
 void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* xc,
-                    double* x, int zident, cudaStream_t st) {
+                    double* x, int zident, cudaStream_t st, double w) {
     dim3 grid((F.n1 + 127) / 128, F.n2);
     g_launches += 1;
-    prolong_kernel<<<grid, 128, 0, st>>>(F, Cl, M, xc, x, zident);
+    prolong_kernel<<<grid, 128, 0, st>>>(F, Cl, M, xc, x, zident, w);
 }
 
 void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* coefF,

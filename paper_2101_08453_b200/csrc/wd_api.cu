@@ -244,6 +244,10 @@ struct wd_ctx {
     bool first_res = false;    // the last cycle's first sweep was the residual variant
     cudaEvent_t ev_res[2] = {};
     double prof[6] = {0, 0, 0, 0, 0, 0};
+    // weight w of the coarse-grid correction lam += w P lam_c: 1 (Eq. (7));
+    // env WD_TEST_CORRECTION_WEIGHT sets another value, only so that the tests
+    // can drive a cycle to divergence and exercise the WD_E_DIVERGED guard
+    double corr_w = 1.0;
 };
 
 namespace wd {
@@ -304,6 +308,8 @@ bool is_device_ptr(const void* p) {
 }
 
 // Staging of host arrays through device memory (pooled per context).
+// A Stage still holding a buffer when it goes out of scope (an early error
+// return before stage_finish) gives the buffer back; nothing is copied out.
 struct Stage {
     wd_ctx* ctx = nullptr;
     int slot = -1;
@@ -313,7 +319,14 @@ struct Stage {
     size_t bytes = 0;
     bool out = false;
     bool staged = false;
+    Stage() = default;
+    Stage(const Stage&) = delete;
+    Stage& operator=(const Stage&) = delete;
+    ~Stage();
 };
+
+void stage_release(Stage& s);
+Stage::~Stage() { stage_release(*this); }
 
 int stage_acquire(wd_ctx* ctx, Stage& s, size_t bytes) {
     if (ctx) {
@@ -372,13 +385,17 @@ int stage_finish(cudaStream_t st, std::initializer_list<Stage*> list) {
         any |= s->staged;
     }
     if (any) CK(cudaStreamSynchronize(st));
-    for (Stage* s : list) {
-        if (!s->staged) continue;
-        if (s->ctx && s->slot >= 0) s->ctx->pool_busy[s->slot] = 0;
-        if (s->own) dfree(s->own);
-        s->staged = false;
-    }
+    for (Stage* s : list) stage_release(*s);
     return WD_OK;
+}
+
+void stage_release(Stage& s) {
+    if (!s.staged) return;
+    if (s.ctx && s.slot >= 0) s.ctx->pool_busy[s.slot] = 0;
+    if (s.own) dfree(s.own);
+    s.own = nullptr;
+    s.slot = -1;
+    s.staged = false;
 }
 
 // ------------------------------------------------------------------ planner
@@ -592,6 +609,25 @@ int sum_ranks(wd_ctx* ctx, const double* in, double* out, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ V-cycle
+// Canonical roles of the level buffers: the iterate in raw[1] (every kernel
+// and TMA map refers to it) and the fused sweep's second buffer raw[4].  The
+// sweeps swap the host-side pointers as they are enqueued or captured; every
+// ABI call that runs sweeps restores the canonical roles on exit, error paths
+// included, so a failed capture or an early return cannot leave a level
+// pointing at the wrong buffer for the next call.
+struct RoleGuard {
+    wd_ctx* ctx;
+    explicit RoleGuard(wd_ctx* c) : ctx(c) {}
+    ~RoleGuard() {
+        if (!ctx) return;
+        for (Part& P : ctx->parts)
+            for (int l = 0; l < ctx->nlev; l++) {
+                P.lev[l].lam = P.lev[l].raw[1];
+                P.lev[l].lam2 = P.lev[l].raw[4];
+            }
+    }
+};
+
 int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st);
 int smooth_end(wd_ctx* ctx, int l, cudaStream_t st);
 
@@ -710,7 +746,7 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st, int first = 0) {
     for (Part& P : ctx->parts) {
         Level& F = P.lev[l];
         Level& C = P.lev[l + 1];
-        launch_prolong(F.L, C.L, F.M, C.lam, F.lam, F.nkept == F.L.n3, st);
+        launch_prolong(F.L, C.L, F.M, C.lam, F.lam, F.nkept == F.L.n3, st, ctx->corr_w);
     }
     RC(exchange(ctx, l, ARR_LAM, 1, st));
     for (int s = 0; s < ctx->opt.post_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
@@ -1125,6 +1161,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
     CK(cudaMallocHost((void**)&ctx->hscal, sizeof(double) * 64));
     CK(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
     apply_tma_prepare();
+    gs_fused_prepare();
     if (o.profile) {
         for (auto& e : ctx->ev_gs) CK(cudaEventCreate(&e));
         for (auto& e : ctx->ev_cyc) CK(cudaEventCreate(&e));
@@ -1446,6 +1483,7 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
     if (opt && opt->coarsest_max_free > 8192)
         return fail(WD_E_INVAL, "coarsest_max_free %d > 8192 (dense inverse)", opt->coarsest_max_free);
     wd_ctx* ctx = new wd_ctx();
+    if (const char* v = getenv("WD_TEST_CORRECTION_WEIGHT")) ctx->corr_w = atof(v);
     int rc = assemble_impl(X, Y, Z, n1, n2, n3, a1, a2, a3, opt, (cudaStream_t)stream, ctx);
     if (rc) {
         char keep[1024];
@@ -1506,11 +1544,17 @@ static int recover_pipelined(wd_ctx* ctx, const double* lambda, const double* u0
     CK(cudaStreamWaitEvent(ctx->pin_s, ev[16], 0));
     CK(cudaStreamWaitEvent(ctx->pout_s, ev[16], 0));
     const size_t nplane = (size_t)n1 * n2, eplane = (size_t)nx * ny;
+    int copied = -1;   // last node row of lambda copied in
     for (int c = 0; c < NCH; c++) {
         const int r0 = (int)((long long)ny * c / NCH), r1 = (int)((long long)ny * (c + 1) / NCH);
         if (r1 <= r0) continue;
-        if (hl) {   // node rows r0 .. r1 (inclusive) of every plane
-            const size_t off = (size_t)r0 * n1, w = (size_t)(r1 + 1 - r0) * n1;
+        // recovering element rows r0 .. r1-1 reads node rows r0 .. r1; each node
+        // row is copied once: a chunk copies the rows after the last one copied
+        // up to r1; row r0 came with an earlier chunk on the same copy stream
+        if (hl) {
+            const int a = copied + 1;
+            copied = r1;
+            const size_t off = (size_t)a * n1, w = (size_t)(r1 + 1 - a) * n1;
             CK(cudaMemcpy2DAsync(dl + off, sizeof(double) * nplane, lambda + off, sizeof(double) * nplane,
                                  sizeof(double) * w, n3, cudaMemcpyHostToDevice, ctx->pin_s));
         }
@@ -1538,8 +1582,7 @@ static int recover_pipelined(wd_ctx* ctx, const double* lambda, const double* u0
     CK(cudaStreamWaitEvent(st, ev[8], 0));
     CK(cudaStreamWaitEvent(st, ev[9], 0));
     CK(cudaStreamSynchronize(st));   // host outputs complete on return
-    for (Stage* x : {&sl, &su0, &su})
-        if (x->staged && x->slot >= 0) ctx->pool_busy[x->slot] = 0;
+    for (Stage* x : {&sl, &su0, &su}) stage_release(*x);
     return WD_OK;
 }
 
@@ -1693,6 +1736,7 @@ int wd_downscale_step(wd_ctx* ctx, const double* u0, double* lambda, int warm, d
 
 int wd_vcycle(wd_ctx* ctx, double* lambda, const double* f, double* rel_res_out, void* stream) {
     if (!ctx || !lambda || !f) return fail(WD_E_INVAL, "NULL argument");
+    RoleGuard roles(ctx);
     cudaStream_t st = (cudaStream_t)stream;
     Stage sl, sf;
     RC(stage_in(ctx, sl, lambda, abi_nodes(ctx), st));
@@ -1714,17 +1758,17 @@ int wd_vcycle(wd_ctx* ctx, double* lambda, const double* f, double* rel_res_out,
         *rel_res_out = fn > 0 ? a / fn : a;
         profile_accumulate(ctx, true, true);
     }
-    Stage so = sl;
-    so.out = true;
-    so.host = lambda;
-    out_nodes(ctx, so.d, st);
+    sl.out = true;
+    sl.host = lambda;
+    out_nodes(ctx, sl.d, st);
     CKL();
-    return stage_finish(st, {&so, &sf});
+    return stage_finish(st, {&sl, &sf});
 }
 
 int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol, double* lambda,
              wd_report* rep, void* stream) {
     if (!ctx || !f || !lambda) return fail(WD_E_INVAL, "NULL argument");
+    RoleGuard roles(ctx);
     if (!(rel_tol > 0.0 && rel_tol < 1.0)) return fail(WD_E_INVAL, "rel_tol must be in (0,1)");
     cudaStream_t st = (cudaStream_t)stream;
     Stage sf, s0, sl;
@@ -1775,6 +1819,9 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
     const double fn = std::sqrt(ctx->hscal[1]);
     int status = WD_E_NOCONV;
     int c = 0;
+    // the last four residuals, the one after cycle 1 and the last one are kept
+    // here (rel_res_hist only reports the first 256 cycles)
+    double ring4[4] = {0.0, 0.0, 0.0, 0.0}, rel1 = 0.0, rel_last = 0.0;
     if (fn == 0.0) {
         for (Part& P : ctx->parts) CK(cudaMemsetAsync(P.lev[0].lam, 0, sizeof(double) * P.lev[0].L.NT, st));
         R.rel_res_hist[0] = 0.0;
@@ -1790,9 +1837,12 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
             const double rel = std::sqrt(ctx->hscal[0]) / fn;
             if (c < 256) R.rel_res_hist[c] = rel;
             if (c == 0) R.rel_res0 = rel;
+            if (c == 1) rel1 = rel;
+            ring4[c & 3] = rel;
+            rel_last = rel;
             if (!std::isfinite(rel)) status = WD_E_NONFINITE;
             else if (rel <= rel_tol) status = WD_OK;
-            else if (c >= 3 && c < 256 && rel > 10.0 * R.rel_res_hist[c - 3]) status = WD_E_DIVERGED;
+            else if (c >= 3 && rel > 10.0 * ring4[(c - 3) & 3]) status = WD_E_DIVERGED;
             else if (c >= ctx->opt.max_cycles) status = WD_E_NOCONV;
             else status = -1;   // continue
             if (status != -1) {
@@ -1813,7 +1863,7 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
             RC(run_split(ctx, 2, st));
             c++;
             profile_accumulate(ctx, true, false);
-            const double prev = c >= 2 && c - 2 < 256 ? R.rel_res_hist[c - 2] : 0.0;
+            const double prev = c >= 2 ? ring4[(c - 2) & 3] : 0.0;
             const bool predicted = prev > 0.0 && rel * (rel / prev) <= rel_tol;
             if (predicted || c >= ctx->opt.max_cycles) {
                 RC(residual_sq(ctx, 0, st));
@@ -1828,10 +1878,9 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
     R.cycles = c;
     R.status = status;
     R.converged = status == WD_OK;
-    const int ch = c < 255 ? c : 255;
-    R.rel_res_final = R.rel_res_hist[ch];
-    if (c >= 2) R.rate = std::pow(R.rel_res_hist[ch] / R.rel_res_hist[1], 1.0 / (ch - 1));
-    else if (c == 1) R.rate = R.rel_res_hist[1] / R.rel_res_hist[0];
+    if (fn != 0.0) R.rel_res_final = rel_last;
+    if (c >= 2) R.rate = std::pow(rel_last / rel1, 1.0 / (c - 1));
+    else if (c == 1) R.rate = rel_last / R.rel_res0;
     out_nodes(ctx, sl.d, st);
     CKL();
     RC(stage_finish(st, {&sf, &s0, &sl}));
@@ -1860,6 +1909,7 @@ long long wd_launch_count(void) { return g_launches.load(); }
 int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out) {
     RC(check_level(ctx, level));
     RC(check_single(ctx));
+    RoleGuard roles(ctx);
     if (reps < 1 || !ms_out) return fail(WD_E_INVAL, "reps < 1 or NULL output");
     if ((which == 2 || which == 3 || which == 6) && level >= ctx->nlev - 1)
         return fail(WD_E_INVAL, "no coarser level");
@@ -1973,6 +2023,7 @@ int wd_apply(wd_ctx* ctx, int level, const double* x, double* y, void* stream) {
 int wd_smooth(wd_ctx* ctx, int level, double* x, const double* f, int sweeps, void* stream) {
     RC(check_level(ctx, level));
     RC(check_single(ctx));
+    RoleGuard roles(ctx);
     cudaStream_t st = (cudaStream_t)stream;
     Level& lv = ctx->parts[0].lev[level];
     const size_t N = nodes_of(lv.L);
@@ -2031,6 +2082,7 @@ int wd_prolong(wd_ctx* ctx, int level, const double* xc, double* x, void* stream
 int wd_coarse_solve(wd_ctx* ctx, const double* f, double* x, void* stream) {
     if (!ctx || !f || !x) return fail(WD_E_INVAL, "NULL argument");
     RC(check_single(ctx));
+    RoleGuard roles(ctx);
     cudaStream_t st = (cudaStream_t)stream;
     Level& lc = ctx->parts[0].lev[ctx->nlev - 1];
     const size_t N = nodes_of(lc.L);

@@ -130,8 +130,9 @@ struct MapDev {
 // zident: the z map of the transition is the identity (fast paths, bitwise equal)
 void launch_restrict(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* r,
                      double* fc, int zident, cudaStream_t st);
+// x += w P xc; w = 1 is Eq. (7) (w != 1 only for the divergence-guard test)
 void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* xc,
-                    double* x, int zident, cudaStream_t st);
+                    double* x, int zident, cudaStream_t st, double w = 1.0);
 // zident: the z map of this transition is the identity (no layer merged);
 // regular interior columns then take an unrolled path (bitwise equal)
 void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* coefF,
@@ -146,6 +147,8 @@ void launch_argmin_bottom(const double* Z, int n, double* pval, long long* pidx,
 // partials (returns their number)
 int launch_gs_fused(const LevDev& L, const double* coef, const double* lin, double* lout,
                     const double* f, cudaStream_t st, double* partial = nullptr);
+// per-device kernel attributes; returns the device's SM count
+int gs_fused_prepare();
 
 // k_io.cu: steps either side of the path
 void launch_build_mesh(const double* zs, int n1, int n2, int n3, double x0, double y0, double dx,

@@ -2,7 +2,11 @@
 same seeded inputs.  Tolerances (BASELINE.json north_star, normalisations of
 DESIGN.md "Parity tolerances"):
   * operator apply, RHS, recovery, stencil entries: <= 1e-12 relative max;
-  * one GS sweep, restriction, prolongation, one V-cycle: <= 1e-11 relative max;
+  * one GS sweep, restriction, prolongation: <= 1e-11 relative max;
+  * one V-cycle: <= 1e-10 relative max (SURVEY 8(c) asked 1e-12; the coarsest
+    direct solves differ -- dense Cholesky in the oracle, an explicit
+    Gauss-Jordan inverse on the GPU, reading C8 -- and agree only to
+    O(cond(K_c) eps), which the prolongation carries into the fine iterate);
   * lambda after both solves reach rel. residual 1e-10: <= 1e-8 relative l2;
   * V-cycle convergence factor within 10 %.
 """
@@ -149,6 +153,8 @@ def test_vcycle_parity(case, wd):
     for c in range(3):
         wd.wd_vcycle(ctx, lam, _t(f))
         lam0 = mg.vcycle(lam0, f)
+        # 1e-10, not 1e-12: Cholesky (oracle) vs Gauss-Jordan inverse (GPU) at
+        # the coarsest level agree to O(cond(K_c) eps) only (reading C8)
         assert rel_max(_n(lam), lam0) <= 1e-10, c
 
 
