@@ -1,0 +1,371 @@
+// k_gs_fused2.cu -- the one-pass four-colour sweep of k_gs_fused.cu with a
+// leaner instruction stream (same schedule, same floating-point operations in
+// the same order, hence bitwise equal to it and to the phased schedule).
+//
+// Smoother: "vertical sweeps of Gauss-Seidel from the bottom up to
+// the top, with red-black ordering horizontally into 4 groups", colours
+// (i mod 2, j mod 2) = (0,0),(1,0),(0,1),(1,1) (reading C7).  The schedule
+// (64 x 8 tiles with a recomputed halo, colour c at virtual plane s - 2c at
+// step s, persistent CTAs with the k-pipeline running across tiles, lambda in
+// a 12-plane shared-memory ring, the 27 couplings of the next node in
+// registers one step ahead) is described in k_gs_fused.cu.
+//
+// Measured there (ncu source counters, Paper-scale level 0): ~440 warp
+// instructions per node update, 52 % of them integer address arithmetic, the
+// SM issue slots half busy and 35 % of the warp samples waiting at the
+// per-step barrier -- the step is as long as the slowest warp's instruction
+// stream plus the exposed coupling-load latency.  This version cuts the
+// instruction stream:
+//   * the lambda ring is filled by the tensor-memory accelerator: one
+//     cp.async.bulk.tensor per plane (box 36 positions x 2 halves x 11 rows,
+//     out-of-grid entries zero-filled), issued by one thread LA planes ahead,
+//     completing on one mbarrier per ring slot -- instead of ~50 instructions
+//     per thread and step of per-pair cp.async address arithmetic;
+//   * coupling addresses: the 28 per-slot base pointers (slot plane, row and
+//     plane shift of the backward neighbour) are kernel parameters, so a load
+//     is one 32-bit node offset (+ the thread's x shift) scaled onto a base
+//     instead of a 64-bit multiply-add chain per load;
+//   * ring addressing: plane slots advance incrementally (no modulo per step).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "wd_internal.cuh"
+
+#include <algorithm>
+#include <atomic>
+
+namespace wd {
+
+namespace {
+
+constexpr int HI = 32;              // positions per parity per tile row (TI = 64 columns)
+constexpr int TI = 2 * HI;
+constexpr int TJ = 8;               // tile rows
+constexpr int SW = HI + 4;          // ring positions per parity per row (columns I0-4 .. I0+TI+3)
+constexpr int RW = 2 * SW;          // ring doubles per row
+constexpr int SH = TJ + 3;          // ring rows J0-1 .. J0+TJ+1
+constexpr int PLD = RW * SH;        // doubles of one TMA box (one plane of the ring)
+constexpr int PL = (PLD + 15) / 16 * 16;   // ring plane pitch (128-byte aligned TMA destinations)
+constexpr int RING = 12;            // planes in the ring (>= LA + 8: colour 3 reads plane s-7)
+constexpr int LAG = 2;              // plane lag between consecutive colours
+constexpr int LA = 4;               // lambda planes loaded ahead
+constexpr unsigned BOX_BYTES = PLD * 8;
+// colour regions: rows per colour (B) and halo columns beyond the 32 aligned ones
+constexpr int B0 = TJ / 2 + 1, B1 = TJ / 2 + 1, B2 = TJ / 2, B3 = TJ / 2;
+constexpr int W0 = B0, W1 = W0 + B1, W2 = W1 + B2, W3 = W2 + B3;   // warp ranges
+constexpr int NHALO = 3 * B0 + 2 * B1 + B2;                          // 29 halo columns
+constexpr int THREADS = 32 * (W3 + 1);                               // 19 warps
+constexpr int SHADOW = 8;
+constexpr size_t SMEM = sizeof(double) * PL * RING + 8 * RING + 128;
+constexpr size_t SMEM_RES = SMEM + sizeof(double) * PL * SHADOW;
+static_assert(NHALO <= 32, "halo columns must fit one warp");
+static_assert(RING >= LA + 8, "ring too short");
+
+__device__ __forceinline__ uint32_t sa(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* b, unsigned parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(sa(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// bounded wait: a copy that never lands (a fault) traps instead of hanging
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    unsigned n = 0;
+    while (!mbar_try(b, parity))
+        if (++n > (1u << 26)) __trap();
+}
+__device__ __forceinline__ void tma4(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3,
+                                     uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sa(dst)),
+        "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(sa(bar))
+        : "memory");
+}
+
+// base pointers of the coupling loads: slot s of node p is kf[s][o(p)];
+// the backward coupling K(p, p - d_s) = K_s[p - d_s] is kb[s][o(p) + x shift]
+// (kb[s] already holds the row / plane shift of -d_s)
+struct KBase {
+    const double* kf[14];
+    const double* kb[14];
+};
+
+template <bool RES>
+__global__ void __launch_bounds__(THREADS, 1)
+gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__ KBase KB,
+                 LevDev L, double* __restrict__ lout, const double* __restrict__ f, int jt0,
+                 int ntx, int ntiles, double* __restrict__ partial) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* ring = reinterpret_cast<double*>(smem_raw + ((128 - (sa(smem_raw) & 127)) & 127));
+    double* shadow = ring + PL * RING;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + PL * (RING + (RES ? SHADOW : 0)));
+    for (int t = threadIdx.x; t < PL * (RING + (RES ? SHADOW : 0)); t += THREADS) ring[t] = 0.0;
+    if (threadIdx.x == 0) {
+        for (int t = 0; t < RING; t++) mbar_init(&full[t], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int c, di, dj;
+    bool inreg = true;
+    if (w < W0) { c = 0; dj = 2 * w; di = 2 * lane; }
+    else if (w < W1) { c = 1; dj = 2 * (w - W0); di = 1 + 2 * lane; }
+    else if (w < W2) { c = 2; dj = 1 + 2 * (w - W1); di = 2 * lane; }
+    else if (w < W3) { c = 3; dj = 1 + 2 * (w - W2); di = 1 + 2 * lane; }
+    else if (lane < 3 * B0) {
+        c = 0; dj = 2 * (lane / 3);
+        const int e = lane % 3;
+        di = e == 0 ? -2 : TI + 2 * e - 2;
+    } else if (lane < 3 * B0 + 2 * B1) {
+        const int q = lane - 3 * B0;
+        c = 1; dj = 2 * (q / 2); di = (q % 2) == 0 ? -1 : TI + 1;
+    } else if (lane < NHALO) {
+        const int q = lane - 3 * B0 - 2 * B1;
+        c = 2; dj = 1 + 2 * q; di = TI;
+    } else { c = 0; dj = 0; di = -10; inreg = false; }
+    const int ci = c & 1;
+    const int li = di + 4, lj = dj + 1;
+    const int so = lj * RW + (li & 1) * SW + (li >> 1);
+    const int sxm = ci ? -SW : SW - 1, sxp = ci ? 1 - SW : SW;
+    const int gxm = ci ? -L.H : L.H - 1, gxp = ci ? 1 - L.H : L.H;
+    const int sk = (int)L.sk;
+    const int n3 = L.n3, nz = L.n3 - 1;
+    const int ntk = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int G = ntk * n3;
+
+    auto origin = [&](int k, int& I0, int& J0) {
+        const int tau = (int)blockIdx.x + k * (int)gridDim.x;
+        const int ty = tau / ntx;
+        I0 = (tau - ty * ntx) * TI;
+        J0 = jt0 + ty * TJ;
+    };
+    bool act = false, wrt = false;
+    int own = 0;   // offset of the thread's column at plane 0 (< NT < 2^31)
+    auto set_tile = [&](int k) {
+        int I0, J0;
+        origin(k, I0, J0);
+        const int i = I0 + di, j = J0 + dj;
+        const int jg = j + L.jg0;
+        act = inreg && i >= 1 && i <= L.n1 - 2 && j >= 1 && j <= L.n2 - 2 && jg >= 1 &&
+              jg <= L.n2g - 2;
+        wrt = act && di >= 0 && di < TI && dj < TJ && j >= L.own0 && j < L.own1;
+        own = act ? (int)loff(L, i, j, 0) : 0;
+    };
+    // TMA producer state (thread 0): the virtual plane gl = kl * n3 + zl
+    int kl = 0, zl = 0, lI0 = 0, lJ0 = 0, lslot = 0;
+    auto issue = [&]() {
+        if (zl == 0) origin(kl, lI0, lJ0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect(&full[lslot], BOX_BYTES);
+        tma4(ring + lslot * PL, &mL, (lI0 >> 1) - 2, 0, zl, lJ0 - 1, &full[lslot]);
+        if (++lslot == RING) lslot = 0;
+        if (++zl == n3) { zl = 0; ++kl; }
+    };
+    __syncthreads();   // ring zeroed, barriers initialised
+    if (threadIdx.x == 0)
+        for (int p = 0; p < LA && p < G; p++) issue();
+
+    double kf[13], kb[13], fv = 0.0, kd = 1.0;
+    auto load_k = [&](int z) {
+        const int o = own + z * sk;
+        const int om = o + gxm, op = o + gxp;
+#pragma unroll
+        for (int sl = 1; sl < 14; sl++) kf[sl - 1] = __ldg(KB.kf[sl] + o);
+#pragma unroll
+        for (int sl = 1; sl < 14; sl++) {
+            const int dx = slot_dx(sl), dz = slot_dz(sl);
+            const int ob = dx > 0 ? om : dx < 0 ? op : o;   // x of the backward neighbour i - dx
+            if (dz) kb[sl - 1] = z > 0 ? __ldg(KB.kb[sl] + ob) : 0.0;
+            else kb[sl - 1] = __ldg(KB.kb[sl] + ob);
+        }
+        fv = __ldg(f + o);
+        kd = __ldg(KB.kf[0] + o);
+    };
+    int kn = 0, zn = 0;
+    if (G > 0) set_tile(0);
+    if (c == 0 && act && G > 0) load_k(0);
+
+    // ring slot of the thread's current virtual plane g (advanced with g)
+    int rg = 0;
+    double rr = 0.0;
+    const int nsteps = G + LAG * 3;
+    for (int s = 0; s < nsteps; s++) {
+        if (threadIdx.x == 0 && s + LA < G) issue();
+        // the newest plane any colour reads at this step is s + 1 (colour 0)
+        if (s + 1 < G) mbar_wait(&full[(s + 1) % RING], ((s + 1) / RING) & 1);
+        if (s == 0 && G > 0) mbar_wait(&full[0], 0);
+        const int g = s - LAG * c;
+        if (g >= 0 && g < G) {
+            const int z = zn;
+            const int rp = rg + 1 == RING ? 0 : rg + 1, rq = rg == 0 ? RING - 1 : rg - 1;
+            double* r0 = ring + rg * PL + so;
+            if (RES && inreg) shadow[(g & (SHADOW - 1)) * PL + so] = *r0;
+            if (z < nz && act) {
+                const double* r1 = ring + rp * PL + so;
+                const double* rm = ring + rq * PL + so;
+                auto sc = [&](int dx, int dy) { return dy * RW + (dx < 0 ? sxm : dx > 0 ? sxp : 0); };
+                double acc = 0.0;
+#pragma unroll
+                for (int sl = 1; sl < 14; sl++) {
+                    const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+                    acc = fma(kf[sl - 1], (dz ? r1 : r0)[sc(dx, dy)], acc);
+                }
+#pragma unroll
+                for (int sl = 1; sl < 14; sl++) {
+                    const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+                    if (dz) {
+                        if (z > 0) acc = fma(kb[sl - 1], rm[sc(-dx, -dy)], acc);
+                    } else {
+                        acc = fma(kb[sl - 1], r0[sc(-dx, -dy)], acc);
+                    }
+                }
+                const double v = (fv - acc) / kd;
+                if (RES && wrt) {
+                    const bool codd = c & 1, chi = c >= 2;
+                    const double* s1 = shadow + ((g + 1) & (SHADOW - 1)) * PL + so;
+                    const double* s0 = shadow + (g & (SHADOW - 1)) * PL + so;
+                    const double* sm = shadow + ((g + SHADOW - 1) & (SHADOW - 1)) * PL + so;
+                    auto oldv = [&](int dx, int dy, int dz) {
+                        const bool sh = (dx == 0 && dy == 0) ? dz < 0 : ((dy & 1) ? chi : codd);
+                        const double* rpp = dz > 0 ? r1 : dz < 0 ? rm : r0;
+                        const double* sp = dz > 0 ? s1 : dz < 0 ? sm : s0;
+                        return (sh ? sp : rpp)[sc(dx, dy)];
+                    };
+                    double q = kd * r0[0];
+#pragma unroll
+                    for (int sl = 1; sl < 14; sl++) {
+                        const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+                        q = fma(kf[sl - 1], oldv(dx, dy, dz), q);
+                    }
+#pragma unroll
+                    for (int sl = 1; sl < 14; sl++) {
+                        const int dx = slot_dx(sl), dy = slot_dy(sl), dz = slot_dz(sl);
+                        if (dz) {
+                            if (z > 0) q = fma(kb[sl - 1], oldv(-dx, -dy, -dz), q);
+                        } else {
+                            q = fma(kb[sl - 1], oldv(-dx, -dy, 0), q);
+                        }
+                    }
+                    const double rv = fv - q;
+                    rr = fma(rv, rv, rr);
+                }
+                *r0 = v;
+                if (wrt) lout[own + z * sk] = v;
+            }
+            rg = rp;
+            if (++zn == n3) {
+                zn = 0;
+                if (++kn < ntk) set_tile(kn);
+            }
+            if (g + 1 < G && zn < nz && act) load_k(zn);
+        } else if (g == -1 && act && G > 0) {
+            load_k(0);
+        }
+        __syncthreads();
+    }
+    if (RES) {
+        __shared__ double wsum[THREADS / 32];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rr += __shfl_down_sync(0xffffffffu, rr, o);
+        if (lane == 0) wsum[w] = rr;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < THREADS / 32; q++) t += wsum[q];
+            partial[blockIdx.x] = t;
+        }
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+
+// lambda of a level as the 4-D tensor (position, half, plane, row) with the
+// ring box of one plane: 36 positions x 2 halves x 1 plane x 11 rows; the
+// position extent is the grid's (ceil(n1/2)), so the padding of a half row
+// and everything outside the grid read as zeros
+int make_ring_map(const LevDev& L, const double* v, void* map) {
+    auto enc = encode_fn2();
+    if (!enc) return -1;
+    cuuint64_t dims[4] = {(cuuint64_t)((L.n1 + 1) / 2), 2, (cuuint64_t)L.n3, (cuuint64_t)L.n2};
+    cuuint64_t str[3] = {(cuuint64_t)L.H * 8, (cuuint64_t)L.sk * 8, (cuuint64_t)L.sj * 8};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    cuuint32_t box[4] = {SW, 2, 1, SH};
+    CUresult r = enc((CUtensorMap*)map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)v, dims, str,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -1;
+}
+
+int gs_fused2_prepare() {
+    static std::atomic<int> nsm_dev[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int nsm = nsm_dev[dev].load(std::memory_order_acquire);
+    if (nsm > 0) return nsm;
+    cudaFuncSetAttribute(gs_fused2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(gs_fused2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RES);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+    nsm_dev[dev].store(nsm, std::memory_order_release);
+    return nsm;
+}
+
+// one sweep lin -> lout (k_gs_fused.cu launch_gs_fused); ring_map: the
+// make_ring_map tensor map of lin
+int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map, double* lout,
+                     const double* f, cudaStream_t st, double* partial) {
+    const int nsm = gs_fused2_prepare();
+    KBase KB;
+    for (int s = 0; s < 14; s++) {
+        const int dx = slot_dx(s), dy = slot_dy(s), dz = slot_dz(s);
+        KB.kf[s] = coef + (i64)s * L.NT;
+        // backward neighbour p - d_s: row j - dy, plane z - dz (x shift per thread)
+        KB.kb[s] = coef + (i64)s * L.NT - (i64)dy * L.sj - (i64)dz * L.sk;
+        (void)dx;
+    }
+    const int jt0 = L.own0 - ((L.own0 + L.jg0) & 1);
+    const int ntx = (L.n1 + TI - 1) / TI, nty = (L.own1 - jt0 + TJ - 1) / TJ;
+    g_launches += 1;
+    const int grid = std::min(ntx * nty, nsm);
+    const CUtensorMap* m = (const CUtensorMap*)ring_map;
+    if (partial)
+        gs_fused2_kernel<true><<<grid, THREADS, SMEM_RES, st>>>(*m, KB, L, lout, f, jt0, ntx,
+                                                                ntx * nty, partial);
+    else
+        gs_fused2_kernel<false><<<grid, THREADS, SMEM, st>>>(*m, KB, L, lout, f, jt0, ntx,
+                                                             ntx * nty, nullptr);
+    return grid;
+}
+
+}  // namespace wd

@@ -137,6 +137,7 @@ struct Level {
     int* dmap = nullptr;      // device: lo/co/pos for 3 directions (y local to the part)
     MapDev M;
     alignas(64) unsigned char tmA[128], tmB[128], tmX[128], tmF[128];
+    alignas(64) unsigned char tmR[2][128];   // ring maps of raw[1] and raw[4] (k_gs_fused2.cu)
 };
 
 struct Part {
@@ -252,6 +253,7 @@ struct wd_ctx {
 
 namespace wd {
 std::atomic<long long> g_launches{0};
+int g_gs_v2 = 1;
 int g_apply_variant = 1;
 int g_galerkin_generic = 0;
 }
@@ -472,10 +474,20 @@ int alloc_level(wd_ctx* ctx, Level& lv) {
     // D entries of the ping-pong buffer stay 0 (the fused sweep writes free nodes only)
     CK(cudaMemset(lv.lam2, 0, sizeof(double) * nt));
     if (make_coef_maps(lv.L, lv.coef, lv.tmA, lv.tmB) || make_vec_map(lv.L, lv.lam, lv.tmX, true) ||
-        make_vec_map(lv.L, lv.f, lv.tmF, false))
+        make_vec_map(lv.L, lv.f, lv.tmF, false) || make_ring_map(lv.L, lv.raw[1], lv.tmR[0]) ||
+        make_ring_map(lv.L, lv.raw[4], lv.tmR[1]))
         return fail(WD_E_CUDA, "cuTensorMapEncodeTiled failed for level dims (%d,%d,%d)", lv.L.n1,
                     lv.L.n2, lv.L.n3);
     return WD_OK;
+}
+
+// one fused sweep lam -> lam2 of a level (k_gs_fused2.cu unless disabled or
+// the level is too large for 32-bit offsets); partial: also ||f - K lam||^2
+int gs_sweep_level(Level& F, cudaStream_t st, double* partial = nullptr) {
+    if (g_gs_v2 && F.L.NT < (1ll << 31) && (F.lam == F.raw[1] || F.lam == F.raw[4]))
+        return launch_gs_fused2(F.L, F.coef, F.tmR[F.lam == F.raw[1] ? 0 : 1], F.lam2, F.f, st,
+                                partial);
+    return launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st, partial);
 }
 
 // residual r = f - K lam (f_on) or r = K lam on level `lv`; optional per-CTA partials
@@ -665,7 +677,7 @@ int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st) {
         RC(exchange(ctx, l, ARR_LAM, 2, st));
         for (Part& P : ctx->parts) {
             Level& F = P.lev[l];
-            launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st);
+            gs_sweep_level(F, st);
             std::swap(F.lam, F.lam2);
         }
     } else {
@@ -708,7 +720,7 @@ int smooth_first_res(wd_ctx* ctx, bool prof, cudaStream_t st) {
     for (size_t p = 0; p < ctx->parts.size(); p++) {
         Part& P = ctx->parts[p];
         Level& F = P.lev[0];
-        const int nb = launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st, P.partial);
+        const int nb = gs_sweep_level(F, st, P.partial);
         std::swap(F.lam, F.lam2);
         launch_reduce_sum(P.partial, nb, per + p, st);
     }
@@ -1162,6 +1174,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
     CK(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
     apply_tma_prepare();
     gs_fused_prepare();
+    gs_fused2_prepare();
     if (o.profile) {
         for (auto& e : ctx->ev_gs) CK(cudaEventCreate(&e));
         for (auto& e : ctx->ev_cyc) CK(cudaEventCreate(&e));
@@ -1471,6 +1484,7 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
     if (const char* v = getenv("WD_APPLY_VARIANT")) g_apply_variant = atoi(v);
     if (const char* v = getenv("WD_TMA_DEBUG")) g_tma_debug = atoi(v);
     g_galerkin_generic = getenv("WD_GALERKIN_GENERIC") ? atoi(getenv("WD_GALERKIN_GENERIC")) : 0;
+    g_gs_v2 = getenv("WD_GS_V2") ? atoi(getenv("WD_GS_V2")) : 1;
     if (!X || !Y || !Z) return fail(WD_E_INVAL, "NULL coordinate array");
     if (n1 < 3 || n2 < 3 || n3 < 2) return fail(WD_E_INVAL, "dims (%d,%d,%d): need n1,n2 >= 3, n3 >= 2", n1, n2, n3);
     if (n3 - 1 >= MAXNZ) return fail(WD_E_INVAL, "n3 = %d exceeds %d", n3, MAXNZ);
@@ -1928,7 +1942,7 @@ int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out)
             case 8: launch_gs_sweep(F.L, F.coef, F.lam, F.f, st); break;
             case 9:   // two fused sweeps of the residual variant, reported per sweep
                 for (int t = 0; t < 2; t++) {
-                    launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st, P.partial);
+                    gs_sweep_level(F, st, P.partial);
                     std::swap(F.lam, F.lam2);
                 }
                 return smooth_end(ctx, level, st);

@@ -149,6 +149,13 @@ int launch_gs_fused(const LevDev& L, const double* coef, const double* lin, doub
                     const double* f, cudaStream_t st, double* partial = nullptr);
 // per-device kernel attributes; returns the device's SM count
 int gs_fused_prepare();
+// k_gs_fused2.cu: the same sweep (bitwise) with a TMA-filled lambda ring and
+// 32-bit coupling offsets (needs NT < 2^31); ring_map = make_ring_map of lin
+extern int g_gs_v2;   // env WD_GS_V2=0: use k_gs_fused.cu
+int make_ring_map(const LevDev& L, const double* v, void* map);
+int gs_fused2_prepare();
+int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map, double* lout,
+                     const double* f, cudaStream_t st, double* partial = nullptr);
 
 // k_io.cu: steps either side of the path
 void launch_build_mesh(const double* zs, int n1, int n2, int n3, double x0, double y0, double dx,
