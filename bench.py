@@ -49,16 +49,52 @@ CPU_CROP = 200                            # oracle sample: 200x200x15 elements o
 def vcycle_hbm(levels, ms, peak, sweeps=4):
     """Whole-V-cycle algorithmic HBM bytes over its measured
     time: per level (free nodes F_l) `sweeps` smoother sweeps x 136 B, the
-    residual 136 B, restriction 8 B + 8 B per coarse node, prolongation
-    16 B + 8 B per coarse node (the coarsest level: dense solve, ignored)."""
+    residual + restriction 128 B (operator, lambda and f read once; the
+    residual itself need not reach HBM), the coarse right-hand side written
+    8 B per coarse node, prolongation 16 B + 8 B per coarse node (the coarsest
+    level: dense solve, ignored)."""
     tot = 0.0
     for l, (n1, n2, n3) in enumerate(levels[:-1]):
         fr = (n1 - 2) * (n2 - 2) * (n3 - 1)
         c1, c2, c3 = levels[l + 1]
         fc = (c1 - 2) * (c2 - 2) * (c3 - 1)
-        tot += fr * (sweeps * 136 + 136 + 8 + 16) + fc * 16
+        tot += fr * (sweeps * 136 + 128 + 16) + fc * 16
     gbs = tot / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
     return {"bytes": tot, "achieved_GBps": gbs, "frac": gbs / peak}
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_fullsize(config):
+    """The oracle's own solve of the whole workload, from the committed
+    GPU-vs-oracle parity run (scripts/parity_fullsize.py, same box type):
+    too long for the bench's bounded sample, quoted here for context."""
+    p = os.path.join(ROOT, "profiles", f"r2_parity_{config}.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        r = json.load(open(p))
+        o = r["oracle"]
+        n1, n2, n3 = r["dims"]
+        nodes = n1 * n2 * n3
+        c8 = o.get("cycles_to_1e8")
+        t = o["time_s"]
+        per_cycle = t["solve"] / max(o["cycles"], 1)
+        return {"source": os.path.relpath(p, ROOT), "threads": r["host"]["oracle_threads"],
+                "cpu_model": r["host"]["cpu_model"], "setup_s": t["setup"] + t["rhs"],
+                "solve_to_1e-10_s": t["solve"], "cycles_to_1e-10": o["cycles"],
+                "cycles_to_1e-8": c8, "time_to_1e-8_s": per_cycle * c8 if c8 else None,
+                "node_cycles_per_s": nodes * o["cycles"] / t["solve"]}
+    except Exception:
+        return None
 
 
 def measured_hbm_peak():
@@ -289,6 +325,7 @@ def run_ours(args, ws, rank, local):
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     parts = np.zeros(4)
     cycles, gs_ms, gs_sweeps, vc_ms, vc_n, rates = 0, 0.0, 0, 0.0, 0, []
+    gsr_ms, gsr_sweeps = 0.0, 0
     with Clocks(local) as clk:
         start.record(stream)
         for _ in range(args.steps):
@@ -299,6 +336,8 @@ def run_ours(args, ws, rank, local):
             rates.append(rep["rate"])
             gs_ms += prof["gs0_ms"]
             gs_sweeps += int(prof["gs0_sweeps"])
+            gsr_ms += prof["gs0res_ms"]
+            gsr_sweeps += int(prof["gs0res_sweeps"])
             vc_ms += prof["vcycle_ms"]
             vc_n += int(prof["vcycles"])
             info = hier_info(ctx)
@@ -322,9 +361,14 @@ def run_ours(args, ws, rank, local):
         free0 = (n1 - 2) * (n2 - 2) * (n3 - 1)
     gs_kind = args.smoother
     gs_b, gs_per_sweep, gs_name = GS_BYTES[gs_kind]
-    launch_ms = gs_ms / max(gs_sweeps, 1) / gs_per_sweep
+    # every level-0 sweep of the timed steps, the residual variant included
+    # (time-weighted: algorithmic bytes of all launches over their total time)
+    n_all = gs_sweeps + gsr_sweeps
+    launch_ms = (gs_ms + gsr_ms) / max(n_all, 1) / gs_per_sweep
     bytes_launch = gs_b * free0
     achieved = bytes_launch / (launch_ms * 1e-3) / 1e9 if launch_ms > 0 else 0.0
+    plain_ms = gs_ms / max(gs_sweeps, 1) / gs_per_sweep
+    res_ms = gsr_ms / max(gsr_sweeps, 1) if gsr_sweeps else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_gs_traffic.json")
     if os.path.exists(tp):
@@ -355,10 +399,18 @@ def run_ours(args, ws, rank, local):
             "ms_per_vcycle": vc_ms / max(vc_n, 1),
             "vcycle_hbm": vcycle_hbm(levels, vc_ms / max(vc_n, 1), peak),
             "device_bytes": dev_bytes,
-            "roofline": {"kernel": f"{gs_name} (level 0)", "bound": "hbm",
+            "roofline": {"kernel": f"{gs_name} (level 0, all sweeps incl. the residual "
+                                   "variant, time-weighted)", "bound": "hbm",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "bytes_per_launch": bytes_launch, "launch_ms": launch_ms,
+                         "launches": n_all * gs_per_sweep,
+                         "plain": {"launch_ms": plain_ms, "launches": gs_sweeps * gs_per_sweep,
+                                   "frac": (bytes_launch / (plain_ms * 1e-3) / 1e9 / peak
+                                            if plain_ms > 0 else None)},
+                         "residual_variant": {"launch_ms": res_ms, "launches": gsr_sweeps,
+                                              "frac": (bytes_launch / (res_ms * 1e-3) / 1e9 / peak
+                                                       if res_ms else None)},
                          "peak_source": peak_src},
             "gpu_launches": int(launches), "clocks": clk.summary(),
         }
@@ -475,9 +527,12 @@ def run_ours(args, ws, rank, local):
             nst += 1
         line["cpu_baseline"] = {
             "value": samp.n_nodes * cyc / tot, "unit": "node-cycles/s",
-            "cores": oracle.num_threads(), "kind": "oracle",
+            "cores": oracle.num_threads(), "cpu_model": cpu_model(), "kind": "oracle",
             "sample": (f"{nst} full steps on the {samp.nx}x{samp.ny}x{samp.nz}-element centre "
                        f"crop ({samp.n_nodes} nodes), {tot:.1f} s")}
+        full_ref = oracle_fullsize(args.config)
+        if full_ref:
+            line["cpu_baseline"]["full_size_note"] = full_ref
     if rank == 0:
         print(json.dumps(line), flush=True)
 

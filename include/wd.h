@@ -213,10 +213,13 @@ int wd_residual_norm(wd_ctx* ctx, const double* x, const double* f, double* abs_
 
 /* Device-side profile gathered while opt.profile = 1 (CUDA events, also inside
  * the captured V-cycle graph), accumulated over wd_solve/wd_vcycle calls:
- *   out[0] ms in level-0 GS sweeps   out[1] level-0 sweeps (4 launches each)
- *   out[2] ms in V-cycles             out[3] V-cycles
- *   out[4] ms in residual-norm passes out[5] residual-norm passes
- * Returns the number of values written (<= n). */
+ *   out[0] ms in plain level-0 sweeps        out[1] their number
+ *   out[2] ms in V-cycles                    out[3] V-cycles
+ *   out[4] ms in residual-norm passes        out[5] residual-norm passes
+ *   out[6] ms in level-0 sweeps that also return the residual of their input
+ *          (the first sweep of a cycle in wd_solve)   out[7] their number
+ * A sweep is one launch of the fused smoother (four launches with
+ * WD_SMOOTH_PHASED).  Returns the number of values written (<= n, <= 8). */
 int wd_profile_read(const wd_ctx* ctx, double* out, int n);
 /* Reset the accumulated profile. */
 void wd_profile_reset(wd_ctx* ctx);

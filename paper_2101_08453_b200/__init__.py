@@ -224,9 +224,10 @@ class Context:
 
 
 def wd_profile_read(ctx: Context):
-    out = (C.c_double * 6)()
-    _lib.wd_profile_read(ctx.h, out, 6)
-    keys = ("gs0_ms", "gs0_sweeps", "vcycle_ms", "vcycles", "resid_ms", "resids")
+    out = (C.c_double * 8)()
+    _lib.wd_profile_read(ctx.h, out, 8)
+    keys = ("gs0_ms", "gs0_sweeps", "vcycle_ms", "vcycles", "resid_ms", "resids", "gs0res_ms",
+            "gs0res_sweeps")
     return dict(zip(keys, list(out)))
 
 

@@ -23,6 +23,7 @@
 
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for nsys / ncu --nvtx
 
 #include <algorithm>
 #include <cmath>
@@ -37,6 +38,24 @@ using namespace wd;
 namespace {
 
 thread_local char g_err[1024] = "";
+
+// NVTX range for the lifetime of a scope (ABI calls, solve cycles, and the
+// V-cycle phases per level when they are enqueued -- with the CUDA graph that
+// is once, at capture; WD_USE_GRAPH-free runs show them on every cycle)
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    Nvtx(const char* fmt, int a) {
+        char b[64];
+        snprintf(b, sizeof b, fmt, a);
+        nvtxRangePushA(b);
+    }
+    ~Nvtx() { end(); }
+    void end() {   // close the range early (once)
+        if (on) nvtxRangePop();
+        on = false;
+    }
+    bool on = true;
+};
 
 int fail(int code, const char* fmt, ...) {
     va_list ap;
@@ -244,7 +263,7 @@ struct wd_ctx {
     cudaEvent_t ev_cyc[2] = {};
     bool first_res = false;    // the last cycle's first sweep was the residual variant
     cudaEvent_t ev_res[2] = {};
-    double prof[6] = {0, 0, 0, 0, 0, 0};
+    double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     // weight w of the coarse-grid correction lam += w P lam_c: 1 (Eq. (7));
     // env WD_TEST_CORRECTION_WEIGHT sets another value, only so that the tests
     // can drive a cycle to divergence and exercise the WD_E_DIVERGED guard
@@ -738,11 +757,19 @@ bool lagged_residual(const wd_ctx* ctx) {
 // first = 1: the first level-0 pre-smoothing sweep has already run
 // (smooth_first_res or smooth), continue the cycle from there
 int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st, int first = 0) {
-    if (l == ctx->nlev - 1) return coarse_solve(ctx, st);
+    Nvtx nv("level %d", l);
+    if (l == ctx->nlev - 1) {
+        Nvtx nc("coarsest solve");
+        return coarse_solve(ctx, st);
+    }
     const bool prof = ctx->opt.profile && l == 0 && ctx->parts.size() == 1;
     int ns = first;
-    for (int s = first; s < ctx->opt.pre_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
-    RC(smooth_end(ctx, l, st));
+    {
+        Nvtx n_("pre-smoothing");
+        for (int s = first; s < ctx->opt.pre_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
+        RC(smooth_end(ctx, l, st));
+    }
+    Nvtx n_res("residual + restriction");
     for (Part& P : ctx->parts) apply_level(P.lev[l], true, nullptr, st);
     RC(exchange(ctx, l, ARR_R, 1, st));
     for (Part& P : ctx->parts) {
@@ -754,13 +781,17 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st, int first = 0) {
     else if (fused_level(ctx, l + 1)) RC(exchange(ctx, l + 1, ARR_F, 1, st));   // halo row of f_c
     for (Part& P : ctx->parts) CK(cudaMemsetAsync(P.lev[l + 1].lam, 0, sizeof(double) * P.lev[l + 1].L.NT, st));
     CKL();
+    n_res.end();
     RC(vcycle_level(ctx, l + 1, st));
+    Nvtx n_pro("prolongation");
     for (Part& P : ctx->parts) {
         Level& F = P.lev[l];
         Level& C = P.lev[l + 1];
         launch_prolong(F.L, C.L, F.M, C.lam, F.lam, F.nkept == F.L.n3, st, ctx->corr_w);
     }
     RC(exchange(ctx, l, ARR_LAM, 1, st));
+    n_pro.end();
+    Nvtx n_post("post-smoothing");
     for (int s = 0; s < ctx->opt.post_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
     RC(smooth_end(ctx, l, st));
     CKL();
@@ -778,10 +809,12 @@ void profile_accumulate(wd_ctx* ctx, bool cycle, bool resid) {
         const int ns = std::min(ctx->opt.pre_smooth + ctx->opt.post_smooth, 16);
         if (ctx->nlev > 1 && ctx->parts.size() == 1)
             // level-0 sweeps of the plain kernel (the residual variant is not counted)
-            for (int s = ctx->first_res ? 1 : 0; s < ns; s++)
+            for (int s = 0; s < ns; s++)
                 if (cudaEventElapsedTime(&ms, ctx->ev_gs[2 * s], ctx->ev_gs[2 * s + 1]) == cudaSuccess) {
-                    ctx->prof[0] += ms;
-                    ctx->prof[1] += 1;
+                    // the residual variant (first sweep of a cycle in wd_solve) apart
+                    const int slot = (s == 0 && ctx->first_res) ? 6 : 0;
+                    ctx->prof[slot] += ms;
+                    ctx->prof[slot + 1] += 1;
                 }
         if (cudaEventElapsedTime(&ms, ctx->ev_cyc[0], ctx->ev_cyc[1]) == cudaSuccess) {
             ctx->prof[2] += ms;
@@ -1479,6 +1512,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
 int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
                 double a1, double a2, double a3, const wd_options* opt, void* stream,
                 wd_ctx** out) {
+    Nvtx nvtx_("wd_assemble");
     if (!out) return fail(WD_E_INVAL, "out is NULL");
     *out = nullptr;
     if (const char* v = getenv("WD_APPLY_VARIANT")) g_apply_variant = atoi(v);
@@ -1515,6 +1549,7 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
 }
 
 int wd_rhs(wd_ctx* ctx, const double* u0, double* f, void* stream) {
+    Nvtx nvtx_("wd_rhs");
     if (!ctx || !u0 || !f) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
     Stage su, sf;
@@ -1601,6 +1636,7 @@ static int recover_pipelined(wd_ctx* ctx, const double* lambda, const double* u0
 }
 
 int wd_recover_wind(wd_ctx* ctx, const double* lambda, const double* u0, double* u, void* stream) {
+    Nvtx nvtx_("wd_recover_wind");
     if (!ctx || !lambda || !u0 || !u) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
     if (ctx->mode == MODE_SINGLE && (!is_device_ptr(lambda) || !is_device_ptr(u0) || !is_device_ptr(u)))
@@ -1726,6 +1762,7 @@ int wd_mass_consistency(wd_ctx* ctx, const double* u, double out[2], void* strea
 
 int wd_downscale_step(wd_ctx* ctx, const double* u0, double* lambda, int warm, double rel_tol,
                       double* u, wd_report* rep, void* stream) {
+    Nvtx nvtx_("wd_downscale_step");
     if (!ctx || !u0 || !lambda || !u) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
     // host arrays cross PCIe once: u0 up, (lambda up when warm), lambda and u down
@@ -1749,6 +1786,7 @@ int wd_downscale_step(wd_ctx* ctx, const double* u0, double* lambda, int warm, d
 }
 
 int wd_vcycle(wd_ctx* ctx, double* lambda, const double* f, double* rel_res_out, void* stream) {
+    Nvtx nvtx_("wd_vcycle");
     if (!ctx || !lambda || !f) return fail(WD_E_INVAL, "NULL argument");
     RoleGuard roles(ctx);
     cudaStream_t st = (cudaStream_t)stream;
@@ -1781,6 +1819,7 @@ int wd_vcycle(wd_ctx* ctx, double* lambda, const double* f, double* rel_res_out,
 
 int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol, double* lambda,
              wd_report* rep, void* stream) {
+    Nvtx nvtx_("wd_solve");
     if (!ctx || !f || !lambda) return fail(WD_E_INVAL, "NULL argument");
     RoleGuard roles(ctx);
     if (!(rel_tol > 0.0 && rel_tol < 1.0)) return fail(WD_E_INVAL, "rel_tol must be in (0,1)");
@@ -1842,6 +1881,7 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
         status = WD_OK;
     } else {
         for (;;) {
+            Nvtx n_cyc("cycle %d", c + 1);
             bool first_done = false;
             if (!have) {   // first sweep of cycle c+1, returning the residual of lam_c
                 RC(run_split(ctx, 0, st));
@@ -1908,7 +1948,7 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
 // ------------------------------------------------------------------ profiling
 int wd_profile_read(const wd_ctx* ctx, double* out, int n) {
     if (!ctx || !out) return 0;
-    int m = n < 6 ? n : 6;
+    int m = n < 8 ? n : 8;
     for (int t = 0; t < m; t++) out[t] = ctx->prof[t];
     return m;
 }
