@@ -174,6 +174,27 @@ void wd_destroy(wd_ctx* ctx);
  * Owned node rows [*j_begin, *j_end) of `rank` among nranks: an even split
  * floor(n2 r / R) .. floor(n2 (r+1) / R).  Every rank must own >= 4 rows. */
 void wd_partition_rows(int n2, int nranks, int rank, int* j_begin, int* j_end);
+/* Host-only inspection of the slab decomposition (SURVEY 8(e)
+ * requirement (1); no device work, callable without a GPU): the hierarchy
+ * wd_assemble builds for these global node dims, penalty constants, options
+ * and planner inputs (h1 = sqrt(dx dy), h3[n3-1] = layer thicknesses of the
+ * minimum-terrain column, reading C2), seen from `rank` of `nranks`.
+ *   *nlevels, *gather (first replicated level, -1: none);
+ *   lev[8 l + 0..2]  global node dims of level l (l < max_levels);
+ *   lev[8 l + 3]     1 if level l is distributed (slab rows), 0 if replicated;
+ *   lev[8 l + 4..5]  global rows [a, b) this rank holds (owned + halo rows);
+ *   lev[8 l + 6..7]  global rows [a, b) it owns (distributed) or computes
+ *                    before the gather (replicated);
+ *   msgs[5 m + 0..4] the messages of one w-row halo exchange (the ncclSend /
+ *                    ncclRecv pairs the V-cycle issues; virtual ranks copy the
+ *                    same rows) on every distributed level: level, peer,
+ *                    1 send / 0 receive, first global row, rows;  *nmsgs.
+ * Returns WD_OK; WD_E_INVAL for bad dims/ranks (also when a rank would own
+ * fewer than 4 rows) or when an output array is too short. */
+int wd_plan_decomposition(int n1, int n2, int n3, double a1, double a2, double a3, double h1,
+                          const double* h3, const wd_options* opt, int nranks, int rank, int w,
+                          int* nlevels, int* gather, int* lev, int max_levels, int* msgs,
+                          int max_msgs, int* nmsgs);
 /* ncclGetUniqueId (libnccl.so.2 is loaded at run time) into id[128]; rank 0
  * calls it and broadcasts the bytes to the other ranks. */
 int wd_nccl_unique_id(char id[128]);

@@ -259,6 +259,38 @@ def slab_rows(n2, nranks, rank, halo=2):
     return max(a - halo, 0), min(b + halo, n2)
 
 
+_lib.wd_plan_decomposition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                       C.c_double, C.c_double, C.POINTER(C.c_double),
+                                       C.POINTER(wd_options), C.c_int, C.c_int, C.c_int,
+                                       C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                       C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int), C.c_int,
+                                       C.POINTER(C.c_int)]
+
+
+def wd_plan_decomposition(dims, a, h1, h3, nranks, rank, w=1, opt: wd_options | None = None):
+    """Host-only slab-decomposition plan (wd.h wd_plan_decomposition): the
+    hierarchy and this rank's rows per level, the gather level and the halo
+    messages of one w-row exchange.  No GPU needed."""
+    n1, n2, n3 = dims
+    h3a = (C.c_double * (n3 - 1))(*[float(v) for v in h3])
+    o = opt if opt is not None else default_options()
+    nl, ga, nm = C.c_int(), C.c_int(), C.c_int()
+    lev = (C.c_int * (8 * 32))()
+    msgs = (C.c_int * (5 * 4 * 32))()
+    _check(_lib.wd_plan_decomposition(int(n1), int(n2), int(n3), float(a[0]), float(a[1]),
+                                      float(a[2]), float(h1), h3a, C.byref(o), int(nranks),
+                                      int(rank), int(w), C.byref(nl), C.byref(ga), lev, 32, msgs,
+                                      4 * 32, C.byref(nm)))
+    levels = []
+    for l in range(nl.value):
+        v = lev[8 * l: 8 * l + 8]
+        levels.append(dict(dims=tuple(v[0:3]), dist=bool(v[3]), held=(v[4], v[5]),
+                           owned=(v[6], v[7])))
+    ms = [dict(level=msgs[5 * m], peer=msgs[5 * m + 1], send=bool(msgs[5 * m + 2]),
+               row0=msgs[5 * m + 3], rows=msgs[5 * m + 4]) for m in range(nm.value)]
+    return dict(nlevels=nl.value, gather=ga.value, levels=levels, msgs=ms)
+
+
 def wd_nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(_lib.wd_nccl_unique_id(buf))

@@ -482,6 +482,152 @@ void coarse_range(const std::vector<int>& pos, int a, int b, int& c0, int& c1) {
     c1 = (int)(std::lower_bound(pos.begin(), pos.end(), b) - pos.begin());
 }
 
+// ------------------------------------------------------------------ host plan
+// The hierarchy and its slab layout, computed on the host from the global
+// dims, the options, the row partition and the planner inputs (h1, h3) --
+// no device work.  wd_assemble builds exactly this plan (then assembles and
+// forms the Galerkin operators on it); wd_plan_decomposition returns it for
+// inspection, so the multi-rank layout and the exchange / gather schedule can
+// be checked without GPUs (tests/test_dist_plan.py).
+struct PartLevel {
+    LevDev L;
+    bool dist = false;
+    int cown0 = 0, cown1 = 0;
+};
+struct HierPlan {
+    int nlev = 0;
+    int gather = MAXLEV;
+    int dims[MAXLEV][3];
+    int hflag[MAXLEV], nkept[MAXLEV];
+    int kept[MAXLEV][MAXNZ];
+    std::vector<int> px[MAXLEV], py[MAXLEV];   // kept fine positions of transition l -> l+1
+    std::vector<std::vector<std::pair<int, int>>> rrows;   // [level][rank] rows owned / computed
+    std::vector<std::vector<PartLevel>> part;              // [part][level]
+    std::vector<int> own0g, own1g;                         // level-0 owned rows per rank
+};
+
+// parts: the ranks whose layout is wanted (all R in virtual mode, this rank
+// with NCCL, {0} on one GPU)
+int plan_hierarchy(int n1, int n2, int n3, const double a[3], const wd_options& o, int nranks,
+                   const std::vector<int>& parts, double h1, const double* h3_in, HierPlan& H) {
+    const bool multi = nranks > 1;
+    H.own0g.resize(nranks);
+    H.own1g.resize(nranks);
+    for (int r = 0; r < nranks; r++) wd_partition_rows(n2, nranks, r, &H.own0g[r], &H.own1g[r]);
+    for (int r = 0; r < nranks; r++)
+        if (H.own1g[r] - H.own0g[r] < MIN_OWNED)
+            return fail(WD_E_INVAL, "rank %d owns %d rows (< %d)", r, H.own1g[r] - H.own0g[r], MIN_OWNED);
+    H.part.assign(parts.size(), std::vector<PartLevel>(MAXLEV));
+    for (size_t p = 0; p < parts.size(); p++) {
+        const int r = parts[p];
+        const int jlo = multi ? std::max(H.own0g[r] - HALO, 0) : 0;
+        const int jhi = multi ? std::min(H.own1g[r] + HALO, n2) : n2;
+        PartLevel& L0 = H.part[p][0];
+        L0.L = make_level(n1, jhi - jlo, n3, jlo, n2, H.own0g[r] - jlo, H.own1g[r] - jlo);
+        L0.dist = multi;
+        L0.cown0 = L0.L.own0;
+        L0.cown1 = L0.L.own1;
+    }
+    H.nlev = 1;
+    H.gather = MAXLEV;
+    H.dims[0][0] = n1;
+    H.dims[0][1] = n2;
+    H.dims[0][2] = n3;
+    H.rrows.assign(1, std::vector<std::pair<int, int>>(nranks));
+    for (int r = 0; r < nranks; r++) H.rrows[0][r] = {H.own0g[r], H.own1g[r]};
+    double h3[MAXNZ], h3n[MAXNZ], h1n;
+    for (int k = 0; k + 1 < n3; k++) h3[k] = h3_in[k];
+    while (H.nlev < MAXLEV) {
+        const int l = H.nlev - 1;
+        const int fn1 = H.dims[l][0], fn2 = H.dims[l][1], fn3 = H.dims[l][2];
+        if (free_count(fn1, fn2, fn3) <= o.coarsest_max_free) break;
+        int hflag, nk;
+        if (!plan_level(h1, h3, fn3 - 1, a, o.coarsen_rule, fn1, fn2, &hflag, H.kept[l], &nk, &h1n, h3n))
+            break;
+        std::vector<int>& px = H.px[l];
+        std::vector<int>& py = H.py[l];
+        px.assign(fn1, 0);
+        py.assign(fn2, 0);
+        int m1, m2;
+        if (hflag) {
+            m1 = horiz_kept(fn1, px.data());
+            m2 = horiz_kept(fn2, py.data());
+        } else {
+            m1 = fn1;
+            m2 = fn2;
+            for (int t = 0; t < m1; t++) px[t] = t;
+            for (int t = 0; t < m2; t++) py[t] = t;
+        }
+        px.resize(m1);
+        py.resize(m2);
+        H.hflag[l] = hflag;
+        H.nkept[l] = nk;
+        const int cl = l + 1;
+        H.dims[cl][0] = m1;
+        H.dims[cl][1] = m2;
+        H.dims[cl][2] = nk;
+        // gather decision (multi-rank): replicate the coarse level when it is
+        // small or when a rank would own fewer than MIN_OWNED rows of it
+        bool coarse_dist = false;
+        H.rrows.resize(cl + 1);
+        H.rrows[cl].resize(nranks);
+        for (int r = 0; r < nranks; r++) {
+            int c0 = 0, c1 = m2;
+            if (l < H.gather) coarse_range(py, H.rrows[l][r].first, H.rrows[l][r].second, c0, c1);
+            H.rrows[cl][r] = {c0, c1};
+        }
+        if (multi && H.gather == MAXLEV) {
+            coarse_dist = (long long)m1 * m2 * nk >= o.gather_below_nodes;
+            for (int r = 0; r < nranks; r++)
+                if (H.rrows[cl][r].second - H.rrows[cl][r].first < MIN_OWNED) coarse_dist = false;
+            if (!coarse_dist) H.gather = cl;
+        }
+        for (size_t p = 0; p < parts.size(); p++) {
+            const PartLevel& F = H.part[p][l];
+            PartLevel& C = H.part[p][cl];
+            // coarse rows this part owns / computes
+            int c0, c1;
+            coarse_range(py, F.L.jg0 + F.L.own0, F.L.jg0 + F.L.own1, c0, c1);
+            if (!F.dist) { c0 = 0; c1 = m2; }   // replicated fine level: everything
+            if (coarse_dist) {
+                const int jlo_c = std::max(c0 - HALO, 0), jhi_c = std::min(c1 + HALO, m2);
+                C.L = make_level(m1, jhi_c - jlo_c, nk, jlo_c, m2, c0 - jlo_c, c1 - jlo_c);
+                C.dist = true;
+                C.cown0 = C.L.own0;
+                C.cown1 = C.L.own1;
+            } else {
+                C.L = make_level(m1, m2, nk, 0, m2, 0, m2);
+                C.dist = false;
+                C.cown0 = c0;   // slice this part computes before the gather
+                C.cown1 = c1;
+            }
+        }
+        H.nlev++;
+        h1 = h1n;
+        for (int t = 0; t + 1 < nk; t++) h3[t] = h3n[t];
+    }
+    return WD_OK;
+}
+
+// The messages of a w-row halo exchange of distributed level l for rank r
+// (the ncclSend/ncclRecv pairs of exchange(); virtual ranks copy the same
+// rows): {peer, send(1)/recv(0), first global row, rows}.
+struct HaloMsg { int peer, send, row0, rows; };
+std::vector<HaloMsg> halo_msgs(const PartLevel& P, int rank, int nranks, int w) {
+    std::vector<HaloMsg> m;
+    if (!P.dist) return m;
+    const int g0 = P.L.jg0 + P.L.own0, g1 = P.L.jg0 + P.L.own1;
+    if (rank > 0) {
+        m.push_back({rank - 1, 1, g0, w});
+        m.push_back({rank - 1, 0, g0 - w, w});
+    }
+    if (rank < nranks - 1) {
+        m.push_back({rank + 1, 1, g1 - w, w});
+        m.push_back({rank + 1, 0, g1, w});
+    }
+    return m;
+}
+
 int alloc_level(wd_ctx* ctx, Level& lv) {
     const size_t nt = (size_t)lv.L.NT;
     double** arr[5] = {&lv.coef, &lv.lam, &lv.f, &lv.r, &lv.lam2};
@@ -538,26 +684,24 @@ double* arr_of(Level& lv, int which) {
 int exchange(wd_ctx* ctx, int l, int which, int w, cudaStream_t st) {
     if (ctx->mode == MODE_SINGLE || !ctx->parts[0].lev[l].dist) return WD_OK;
     const int np = which == ARR_COEF ? 14 : 1;
+    auto pl_of = [](Level& lv) {
+        PartLevel q;
+        q.L = lv.L;
+        q.dist = lv.dist;
+        return q;
+    };
     if (ctx->mode == MODE_VIRTUAL) {
+        // every send of part p lands in the same global rows of its peer part
         const int R = (int)ctx->parts.size();
         for (int p = 0; p < R; p++) {
             Level& me = ctx->parts[p].lev[l];
-            const LevDev& L = me.L;
-            for (int pl = 0; pl < np; pl++) {
-                const double* src = arr_of(me, which) + (i64)pl * L.NT;
-                if (p > 0) {
-                    Level& dn = ctx->parts[p - 1].lev[l];
-                    double* dst = arr_of(dn, which) + (i64)pl * dn.L.NT;
-                    CK(cudaMemcpyAsync(dst + (i64)dn.L.own1 * dn.L.sj, src + (i64)L.own0 * L.sj,
-                                       sizeof(double) * w * L.sj, cudaMemcpyDeviceToDevice, st));
-                }
-                if (p < R - 1) {
-                    Level& up = ctx->parts[p + 1].lev[l];
-                    double* dst = arr_of(up, which) + (i64)pl * up.L.NT;
-                    CK(cudaMemcpyAsync(dst + (i64)(up.L.own0 - w) * up.L.sj,
-                                       src + (i64)(L.own1 - w) * L.sj, sizeof(double) * w * L.sj,
-                                       cudaMemcpyDeviceToDevice, st));
-                }
+            for (const HaloMsg& m : halo_msgs(pl_of(me), p, R, w)) {
+                if (!m.send) continue;
+                Level& to = ctx->parts[m.peer].lev[l];
+                for (int pl = 0; pl < np; pl++)
+                    CK(cudaMemcpyAsync(arr_of(to, which) + (i64)pl * to.L.NT + (i64)(m.row0 - to.L.jg0) * to.L.sj,
+                                       arr_of(me, which) + (i64)pl * me.L.NT + (i64)(m.row0 - me.L.jg0) * me.L.sj,
+                                       sizeof(double) * m.rows * me.L.sj, cudaMemcpyDeviceToDevice, st));
             }
         }
         return WD_OK;
@@ -566,17 +710,15 @@ int exchange(wd_ctx* ctx, int l, int which, int w, cudaStream_t st) {
     Nccl& N = nccl();
     Level& me = ctx->parts[0].lev[l];
     const LevDev& L = me.L;
-    const size_t cnt = (size_t)w * L.sj;
+    const std::vector<HaloMsg> msgs = halo_msgs(pl_of(me), ctx->rank, ctx->nranks, w);
     NK(N.GroupStart());
     for (int pl = 0; pl < np; pl++) {
         double* a = arr_of(me, which) + (i64)pl * L.NT;
-        if (ctx->rank > 0) {
-            NK(N.Send(a + (i64)L.own0 * L.sj, cnt, ncclDouble, ctx->rank - 1, ctx->comm, st));
-            NK(N.Recv(a + (i64)(L.own0 - w) * L.sj, cnt, ncclDouble, ctx->rank - 1, ctx->comm, st));
-        }
-        if (ctx->rank < ctx->nranks - 1) {
-            NK(N.Send(a + (i64)(L.own1 - w) * L.sj, cnt, ncclDouble, ctx->rank + 1, ctx->comm, st));
-            NK(N.Recv(a + (i64)L.own1 * L.sj, cnt, ncclDouble, ctx->rank + 1, ctx->comm, st));
+        for (const HaloMsg& m : msgs) {
+            double* buf = a + (i64)(m.row0 - L.jg0) * L.sj;
+            const size_t cnt = (size_t)m.rows * L.sj;
+            if (m.send) NK(N.Send(buf, cnt, ncclDouble, m.peer, ctx->comm, st));
+            else NK(N.Recv(buf, cnt, ncclDouble, m.peer, ctx->comm, st));
         }
     }
     NK(N.GroupEnd());
@@ -1101,6 +1243,47 @@ void wd_partition_rows(int n2, int nranks, int rank, int* j_begin, int* j_end) {
     *j_end = (int)((long long)n2 * (rank + 1) / nranks);
 }
 
+int wd_plan_decomposition(int n1, int n2, int n3, double a1, double a2, double a3, double h1,
+                          const double* h3, const wd_options* opt, int nranks, int rank, int w,
+                          int* nlevels, int* gather, int* lev, int max_levels, int* msgs,
+                          int max_msgs, int* nmsgs) {
+    if (!h3 || !nlevels || !gather || !lev || !msgs || !nmsgs) return fail(WD_E_INVAL, "NULL argument");
+    if (n1 < 3 || n2 < 3 || n3 < 2 || n3 - 1 >= MAXNZ) return fail(WD_E_INVAL, "bad dims");
+    if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks || w < 1 || w > HALO)
+        return fail(WD_E_INVAL, "bad nranks / rank / w");
+    wd_options o;
+    if (opt) o = *opt;
+    else wd_default_options(&o);
+    const double a[3] = {a1, a2, a3};
+    HierPlan H;
+    RC(plan_hierarchy(n1, n2, n3, a, o, nranks, std::vector<int>{rank}, h1, h3, H));
+    if (H.nlev > max_levels) return fail(WD_E_INVAL, "max_levels %d < %d levels", max_levels, H.nlev);
+    *nlevels = H.nlev;
+    *gather = H.gather < MAXLEV ? H.gather : -1;
+    int nm = 0;
+    for (int l = 0; l < H.nlev; l++) {
+        const PartLevel& P = H.part[0][l];
+        int* v = lev + 8 * l;
+        for (int d = 0; d < 3; d++) v[d] = H.dims[l][d];
+        v[3] = P.dist ? 1 : 0;
+        v[4] = P.L.jg0;
+        v[5] = P.L.jg0 + P.L.n2;
+        v[6] = P.dist ? P.L.jg0 + P.L.own0 : P.cown0;
+        v[7] = P.dist ? P.L.jg0 + P.L.own1 : P.cown1;
+        for (const HaloMsg& m : halo_msgs(P, rank, nranks, w)) {
+            if (nm >= max_msgs) return fail(WD_E_INVAL, "max_msgs %d too small", max_msgs);
+            int* q = msgs + 5 * nm++;
+            q[0] = l;
+            q[1] = m.peer;
+            q[2] = m.send;
+            q[3] = m.row0;
+            q[4] = m.rows;
+        }
+    }
+    *nmsgs = nm;
+    return WD_OK;
+}
+
 int ensure_pipe(wd_ctx* ctx);
 
 static int assemble_impl(const double* X, const double* Y, const double* Z, int n1, int n2, int n3,
@@ -1296,7 +1479,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
     PT.mark("level-0 assembly");
     // ---- planner inputs (reading C2): h1 = sqrt(dx dy); h3 at the column of minimum Z(i,j,0)
     double h1;
-    double h3[MAXNZ], h3n[MAXNZ], h1n;
+    double h3[MAXNZ];
     {
         Part& P0 = ctx->parts[0];
         double v[4];
@@ -1372,73 +1555,42 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
     }
 
     PT.mark("planner inputs");
-    // ---- hierarchy
-    while (ctx->nlev < MAXLEV) {
-        const int l = ctx->nlev - 1;
-        const int fn1 = ctx->levdims[l][0], fn2 = ctx->levdims[l][1], fn3 = ctx->levdims[l][2];
-        if (free_count(fn1, fn2, fn3) <= o.coarsest_max_free) break;
-        int hflag, kept[MAXNZ], nk;
-        if (!plan_level(h1, h3, fn3 - 1, ctx->a, o.coarsen_rule, fn1, fn2, &hflag, kept, &nk, &h1n, h3n))
-            break;
-        std::vector<int> px(fn1), py(fn2);
-        int m1, m2;
-        if (hflag) {
-            m1 = horiz_kept(fn1, px.data());
-            m2 = horiz_kept(fn2, py.data());
-        } else {
-            m1 = fn1;
-            m2 = fn2;
-            for (int t = 0; t < m1; t++) px[t] = t;
-            for (int t = 0; t < m2; t++) py[t] = t;
+    // ---- hierarchy: the host plan, then per
+    // transition the coarse level's storage, its maps and the Galerkin product
+    HierPlan H;
+    {
+        std::vector<int> prank;
+        for (Part& P : ctx->parts) prank.push_back(P.rank);
+        RC(plan_hierarchy(n1, n2, n3, ctx->a, o, ctx->nranks, prank, h1, h3, H));
+        for (size_t p = 0; p < ctx->parts.size(); p++) {   // level 0 as laid out above
+            const LevDev &a = ctx->parts[p].lev[0].L, &b = H.part[p][0].L;
+            if (a.n2 != b.n2 || a.jg0 != b.jg0 || a.own0 != b.own0 || a.own1 != b.own1)
+                return fail(WD_E_INTERNAL, "level-0 layout differs from the host plan");
         }
-        px.resize(m1);
-        py.resize(m2);
+    }
+    ctx->gather = H.gather;
+    ctx->rrows = H.rrows;
+    for (int l = 0; l + 1 < H.nlev; l++) {
         const int cl = l + 1;
-        ctx->levdims[cl][0] = m1;
-        ctx->levdims[cl][1] = m2;
-        ctx->levdims[cl][2] = nk;
-        // gather decision (multi-rank): replicate the coarse level when it is
-        // small or when a rank would own fewer than MIN_OWNED rows of it
-        bool coarse_dist = false;
-        ctx->rrows.resize(cl + 1);
-        ctx->rrows[cl].resize(ctx->nranks);
-        for (int r = 0; r < ctx->nranks; r++) {
-            int a = 0, b = m2;
-            if (l < ctx->gather) coarse_range(py, ctx->rrows[l][r].first, ctx->rrows[l][r].second, a, b);
-            ctx->rrows[cl][r] = {a, b};
-        }
-        if (multi && ctx->gather == MAXLEV) {
-            coarse_dist = (long long)m1 * m2 * nk >= o.gather_below_nodes;
-            for (int r = 0; r < ctx->nranks; r++)
-                if (ctx->rrows[cl][r].second - ctx->rrows[cl][r].first < MIN_OWNED) coarse_dist = false;
-            if (!coarse_dist) ctx->gather = cl;
-        }
-        for (Part& P : ctx->parts) {
+        const int fn1 = H.dims[l][0], fn2 = H.dims[l][1], fn3 = H.dims[l][2];
+        const int m1 = H.dims[cl][0], m2 = H.dims[cl][1], nk = H.dims[cl][2];
+        const int* kept = H.kept[l];
+        const std::vector<int>& px = H.px[l];
+        const std::vector<int>& py = H.py[l];
+        for (int d = 0; d < 3; d++) ctx->levdims[cl][d] = H.dims[cl][d];
+        for (size_t p = 0; p < ctx->parts.size(); p++) {
+            Part& P = ctx->parts[p];
             Level& F = P.lev[l];
-            F.hflag = hflag;
+            F.hflag = H.hflag[l];
             F.nkept = nk;
             for (int t = 0; t < nk; t++) F.kept[t] = kept[t];
             Level& C = P.lev[cl];
-            // coarse rows this part owns / computes
-            int c0, c1;
-            coarse_range(py, F.L.jg0 + F.L.own0, F.L.jg0 + F.L.own1, c0, c1);
-            if (!F.dist) { c0 = 0; c1 = m2; }   // replicated fine level: everything
-            int jlo_c, jhi_c;
-            if (coarse_dist) {
-                jlo_c = std::max(c0 - HALO, 0);
-                jhi_c = std::min(c1 + HALO, m2);
-                C.L = make_level(m1, jhi_c - jlo_c, nk, jlo_c, m2, c0 - jlo_c, c1 - jlo_c);
-                C.dist = true;
-                C.cown0 = C.L.own0;
-                C.cown1 = C.L.own1;
-            } else {
-                jlo_c = 0;
-                jhi_c = m2;
-                C.L = make_level(m1, m2, nk, 0, m2, 0, m2);
-                C.dist = false;
-                C.cown0 = c0;   // slice this part computes before the gather
-                C.cown1 = c1;
-            }
+            const PartLevel& pc = H.part[p][cl];
+            C.L = pc.L;
+            C.dist = pc.dist;
+            C.cown0 = pc.cown0;
+            C.cown1 = pc.cown1;
+            const int jlo_c = C.L.jg0;
             RC(alloc_level(ctx, C));
             // maps: x and z global; y local to the part (fine rows F.jg0.., coarse rows jlo_c..)
             const int fr = F.L.n2, cr = C.L.n2;
@@ -1477,10 +1629,8 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
             CKL();
         }
         ctx->nlev++;
-        if (coarse_dist) RC(exchange(ctx, cl, ARR_COEF, HALO, st));
+        if (H.part[0][cl].dist) RC(exchange(ctx, cl, ARR_COEF, HALO, st));
         else if (cl == ctx->gather) RC(gather_rows(ctx, cl, ARR_COEF, st));
-        h1 = h1n;
-        for (int t = 0; t + 1 < nk; t++) h3[t] = h3n[t];
     }
     PT.mark("hierarchy (plan+Galerkin)");
     // ---- coarsest level (reading C8): replicated or single
