@@ -308,6 +308,7 @@ class MG:
         if not self.h:
             raise RuntimeError(f"orc_mg_setup failed, err={err.value}")
         L.orc_mg_set_smoother(self.h, SMOOTHERS[smoother])
+        L.orc_mg_set_level_smoother.argtypes = [C.c_void_p, C.c_int, C.c_int]
         self.nlev = L.orc_mg_nlevels(self.h)
         self.coarse_direct = bool(L.orc_mg_coarse_direct(self.h))
         self.dims = []
@@ -324,8 +325,15 @@ class MG:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_mg_free(self.h)
+            try:
+                lib().orc_mg_free(self.h)
+            except TypeError:   # interpreter shutdown: module globals already gone
+                pass
             self.h = None
+
+    def set_level_smoother(self, l, smoother):
+        """Per-level smoother override ("gs" | "line" | None = the hierarchy's)."""
+        lib().orc_mg_set_level_smoother(self.h, int(l), -1 if smoother is None else SMOOTHERS[smoother])
 
     def shape(self, l):
         n1, n2, n3 = self.dims[l]

@@ -745,6 +745,7 @@ typedef struct {
     int nkept;
     int kept[ORC_MAXNZ];
     int *lo[3], *co[3];  /* fine-index maps per direction (size n_d) */
+    int smoother;        /* -1: the hierarchy's smoother; else 0 point GS, 1 line relaxation */
 } orc_level;
 
 typedef struct {
@@ -768,12 +769,17 @@ static i64 level_free(int n1, int n2, int n3) { return (i64)(n1 - 2) * (n2 - 2) 
 
 /* one sweep of the hierarchy's smoother on level l */
 static void mg_smooth(const orc_mg* mg, const orc_level* l, double* x, const double* f) {
-    if (mg->smoother == 1) orc_line_sweep(l->K, l->n1, l->n2, l->n3, x, f);
+    const int sm = l->smoother >= 0 ? l->smoother : mg->smoother;
+    if (sm == 1) orc_line_sweep(l->K, l->n1, l->n2, l->n3, x, f);
     else orc_gs_sweep(l->K, l->n1, l->n2, l->n3, x, f);
 }
 
 /* select the smoother (0 point GS, 1 vertical line relaxation) */
 void orc_mg_set_smoother(orc_mg* mg, int smoother) { mg->smoother = smoother; }
+/* per-level override (SURVEY 8(f) f1 "per-level decisions"); -1 = the global choice */
+void orc_mg_set_level_smoother(orc_mg* mg, int l, int smoother) {
+    if (l >= 0 && l < mg->nlev) mg->L[l].smoother = smoother;
+}
 
 /* parents of fine index t along direction d of level l: returns count (1|2) */
 static inline int parents(const orc_level* l, int d, int t, int* pc, double* pw) {
@@ -985,6 +991,7 @@ static void alloc_level(orc_level* l, int n1, int n2, int n3) {
     l->f = (double*)calloc((size_t)N, sizeof(double));
     l->r = (double*)calloc((size_t)N, sizeof(double));
     for (int d = 0; d < 3; d++) { l->lo[d] = NULL; l->co[d] = NULL; }
+    l->smoother = -1;
 }
 
 void orc_mg_free(orc_mg* mg) {
