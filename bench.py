@@ -296,11 +296,13 @@ def run_ours(args, ws, rank, local):
                              full.Z[:, lo:hi].contiguous(),
                              full.u0[:, :, lo:hi - 1].contiguous(), full.a, dict(full.meta))
         del full
-        opt = wd.default_options(profile=1, coarsen_rule=args.rule, smoother=args.smoother, nranks=ws, rank=rank,
+        opt = wd.default_options(profile=1, coarsen_rule=args.rule, smoother=args.smoother,
+                                 line_from_level=args.line_from, nranks=ws, rank=rank,
                                  nccl_comm=comm, j_begin=jb, j_end=je)
     else:
         prob = full
-        opt = wd.default_options(profile=1, coarsen_rule=args.rule, smoother=args.smoother)
+        opt = wd.default_options(profile=1, coarsen_rule=args.rule, smoother=args.smoother,
+                                 line_from_level=args.line_from)
     # one fixed global grid at every N (split into N slabs for N > 1): total work fixed
     scaling = "strong"
 
@@ -387,6 +389,7 @@ def run_ours(args, ws, rank, local):
             "config": {"workload": CONFIG_NAMES[args.config], "nodes": nodes,
                        "elements": prob.nx * prob.ny * prob.nz, "free_unknowns": free0,
                        "a": list(prob.a), "rel_tol": args.tol, "coarsen_rule": args.rule,
+                       "smoother": args.smoother, "line_from_level": args.line_from,
                        "levels": levels, "plans_horizontal": [p["horizontal"] for p in plans],
                        "step": "wd_assemble + wd_rhs + wd_solve(zero start) + wd_recover_wind",
                        "l2": "inputs larger than L2 (no flush)",
@@ -548,10 +551,16 @@ def main():
     ap.add_argument("--rule", default="coupling_cur",
                     choices=["coupling_cur", "coupling_paper", "verbatim", "full"])
     ap.add_argument("--smoother", default="fused", choices=["fused", "phased"])
+    ap.add_argument("--line-from", type=int, default=None,
+                    help="vertical line relaxation on levels >= this (-1: none; default: the "
+                         "library's wd_default_options)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--warm", type=int, default=10, help="warm-start steps (configs[4]); 0 = off")
     args = ap.parse_args()
+    if args.line_from is None:
+        import paper_2101_08453_b200 as wd
+        args.line_from = wd.default_options().line_from_level
     ws, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, ws, rank)

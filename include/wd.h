@@ -101,6 +101,10 @@ typedef struct {
                                 wd_partition_rows(n2, nranks, rank) */
     int profile;             /* 1: CUDA events around level-0 smoothing and each V-cycle (default 0) */
     int smoother;            /* WD_SMOOTH_* (default WD_SMOOTH_FUSED) */
+    int line_from_level;     /* per-level smoother (SURVEY 8(f) f1 "per-level decisions"):
+                                vertical line relaxation (the WD_SMOOTH_LINE sweep) on the
+                                levels >= this one, `smoother` below it; -1 = `smoother` on
+                                every level (default -1) */
 } wd_options;
 
 typedef struct {

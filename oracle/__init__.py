@@ -297,7 +297,7 @@ class MG:
     """Oracle multigrid hierarchy on one mesh."""
 
     def __init__(self, X, Y, Z, a, rule="coupling_cur", coarsest_max_free=4096, pre=2,
-                 post=2, smoother="gs"):
+                 post=2, smoother="gs", line_from_level=-1):
         self._keep = [_f64(X), _f64(Y), _f64(Z)]
         n3, n2, n1 = X.shape
         err = C.c_int(0)
@@ -310,6 +310,9 @@ class MG:
         L.orc_mg_set_smoother(self.h, SMOOTHERS[smoother])
         L.orc_mg_set_level_smoother.argtypes = [C.c_void_p, C.c_int, C.c_int]
         self.nlev = L.orc_mg_nlevels(self.h)
+        if line_from_level >= 0:   # per-level smoother
+            for l in range(line_from_level, self.nlev):
+                self.set_level_smoother(l, "line")
         self.coarse_direct = bool(L.orc_mg_coarse_direct(self.h))
         self.dims = []
         for l in range(self.nlev):

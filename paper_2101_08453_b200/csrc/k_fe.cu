@@ -223,70 +223,69 @@ assemble_kernel(const double* __restrict__ X, const double* __restrict__ Y,
 
 // ------------------------------------------------------------------ RHS
 // f_p = sum_{e ni p} fe_a(p),  fe_a = -8 detJ(0) gradN_a(0).u0_e
-//     = -detJ(0) sum_d s_ad (Ji(0) u0_e)_d          (dN_a/dxi_d(0) = s_ad/8)
+//     = -detJ(0) sum_d s_ad (Ji(0) u0_e)_d = -(s_a . h_e),  h_e = detJ(0) Ji(0) u0_e
+// (dN_a/dxi_d(0) = s_ad/8).  Per element only the 3-vector h_e is needed: a
+// node at local corner (da, db) of the four elements of one element layer
+// gets from them -(S - T) as their bottom node and -(S + T) as their top node,
+// S = sum_e (s_x hx + s_y hy), T = sum_e hz, s_x = 2 da - 1, s_y = 2 db - 1.
+// A CTA computes TX x TY element columns (1-element halo recomputed) upward in
+// k; h goes through a double-buffered shared plane, so one barrier per layer.
 // Coordinates: the level's local rows; u0 / f: ABI arrays (Nat); f is written
 // on the owned rows only, 0 on the Dirichlet set.
-__global__ void __launch_bounds__(NTH)
+constexpr int RTX = 32, RTY = 16, RNTH = RTX * RTY;
+__global__ void __launch_bounds__(RNTH)
 rhs_kernel(const double* __restrict__ X, const double* __restrict__ Y,
            const double* __restrict__ Z, LevDev L, Nat u0, Nat f) {
-    __shared__ double fe[8][NTH];
+    __shared__ double hs[2][3][RNTH];
     const int n1 = L.n1, n2 = L.n2, n3 = L.n3;
     const int t = threadIdx.x;
-    const int tx = t % TX, ty = t / TX;
-    const int i0 = blockIdx.x * (TX - 1), j0 = blockIdx.y * (TY - 1);
+    const int tx = t % RTX, ty = t / RTX;
+    const int i0 = blockIdx.x * (RTX - 1), j0 = blockIdx.y * (RTY - 1);
     const int ei = i0 - 1 + tx, ej = j0 - 1 + ty;
     const int nx = n1 - 1, ny = n2 - 1, nz = n3 - 1;
     const bool ev = ei >= 0 && ei < nx && ej >= 0 && ej < ny;
     const int ni = i0 + tx, nj = j0 + ty;
-    const bool nv = tx < TX - 1 && ty < TY - 1 && ni < n1 && nj >= L.own0 && nj < L.own1;
+    const bool nv = tx < RTX - 1 && ty < RTY - 1 && ni < n1 && nj >= L.own0 && nj < L.own1;
     const bool ndir = ni == 0 || ni == n1 - 1 || row_dirichlet(L, nj);
     const i64 EC = (i64)nz * u0.n2a * nx;   // one component of the element array
     double* fo = const_cast<double*>(f.p);
     double x[8][3];
     if (ev) load_plane(X, Y, Z, n1, n2, ei, ej, 0, x, 0);
-    double top = 0.0;   // contributions to node level ek from element level ek-1
+    double top = 0.0;   // contribution to node level ek from element level ek-1
     for (int ek = 0; ek < nz; ek++) {
-        double v[8];
+        double h0 = 0.0, h1 = 0.0, h2 = 0.0;
         if (ev) {
             load_plane(X, Y, Z, n1, n2, ei, ej, ek + 1, x, 1);
             const i64 e = ((i64)ek * u0.n2a + ej + u0.jofs) * nx + ei;
             const double u = __ldg(u0.p + e), w1 = __ldg(u0.p + EC + e), w2 = __ldg(u0.p + 2 * EC + e);
             double Ji[3][3];
             const double det = centre_jacobian(x, Ji);
-            double g[3];
-#pragma unroll
-            for (int d = 0; d < 3; d++) g[d] = Ji[d][0] * u + Ji[d][1] * w1 + Ji[d][2] * w2;
-#pragma unroll
-            for (int a = 0; a < 8; a++)
-                v[a] = -det * (sgn(a, 0) * g[0] + sgn(a, 1) * g[1] + sgn(a, 2) * g[2]);
+            h0 = det * (Ji[0][0] * u + Ji[0][1] * w1 + Ji[0][2] * w2);
+            h1 = det * (Ji[1][0] * u + Ji[1][1] * w1 + Ji[1][2] * w2);
+            h2 = det * (Ji[2][0] * u + Ji[2][1] * w1 + Ji[2][2] * w2);
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 x[q][0] = x[q + 4][0];
                 x[q][1] = x[q + 4][1];
                 x[q][2] = x[q + 4][2];
             }
-        } else {
-#pragma unroll
-            for (int a = 0; a < 8; a++) v[a] = 0.0;
         }
-#pragma unroll
-        for (int a = 0; a < 8; a++) fe[a][t] = v[a];
+        double* hb = &hs[ek & 1][0][0];
+        hb[t] = h0;
+        hb[RNTH + t] = h1;
+        hb[2 * RNTH + t] = h2;
         __syncthreads();
         if (nv) {
-            double s = top, s2 = 0.0;
-#pragma unroll
-            for (int ey = 0; ey < 2; ey++)
-#pragma unroll
-                for (int ex = 0; ex < 2; ex++) {
-                    const int te = t + ex + ey * TX;
-                    const int a = (1 - ex) + 2 * (1 - ey);
-                    s += fe[a][te];
-                    s2 += fe[a + 4][te];
-                }
-            fo[((i64)ek * f.n2a + nj + f.jofs) * n1 + ni] = ndir ? 0.0 : s;
-            top = s2;
+            // elements (ex, ey) of the node's 2 x 2: threads t + ex + ey RTX;
+            // the node is their corner (1 - ex, 1 - ey): s_x = 1 - 2 ex, s_y = 1 - 2 ey
+            const int t00 = t, t10 = t + 1, t01 = t + RTX, t11 = t + RTX + 1;
+            const double S = (hb[t00] - hb[t10] + hb[t01] - hb[t11]) +
+                             (hb[RNTH + t00] + hb[RNTH + t10] - hb[RNTH + t01] - hb[RNTH + t11]);
+            const double T = (hb[2 * RNTH + t00] + hb[2 * RNTH + t10]) +
+                             (hb[2 * RNTH + t01] + hb[2 * RNTH + t11]);
+            fo[((i64)ek * f.n2a + nj + f.jofs) * n1 + ni] = ndir ? 0.0 : top - (S - T);
+            top = -(S + T);
         }
-        __syncthreads();
     }
     if (nv) fo[((i64)nz * f.n2a + nj + f.jofs) * n1 + ni] = 0.0;   // top plane is Dirichlet
 }
@@ -365,9 +364,9 @@ int assemble_rows_needed(int t) { return t * (TY - 1) + TY; }   // node rows [0,
 
 void launch_rhs(const double* X, const double* Y, const double* Z, const LevDev& L, Nat u0, Nat f,
                 cudaStream_t st) {
-    dim3 grid((L.n1 + TX - 2) / (TX - 1), (L.n2 + TY - 2) / (TY - 1));
+    dim3 grid((L.n1 + RTX - 2) / (RTX - 1), (L.n2 + RTY - 2) / (RTY - 1));
     g_launches += 1;
-    rhs_kernel<<<grid, NTH, 0, st>>>(X, Y, Z, L, u0, f);
+    rhs_kernel<<<grid, RNTH, 0, st>>>(X, Y, Z, L, u0, f);
 }
 
 void launch_recover(const double* X, const double* Y, const double* Z, const LevDev& L,

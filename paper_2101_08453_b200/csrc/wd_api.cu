@@ -821,8 +821,13 @@ int coarse_solve(wd_ctx* ctx, cudaStream_t st) {
 }
 
 // does level l use the fused one-pass sweep (k_gs_fused.cu)?
-bool fused_level(const wd_ctx* ctx, int l) { return ctx->opt.smoother == WD_SMOOTH_FUSED; }
-bool line_level(const wd_ctx* ctx, int l) { return ctx->opt.smoother == WD_SMOOTH_LINE; }
+bool line_level(const wd_ctx* ctx, int l) {
+    return ctx->opt.smoother == WD_SMOOTH_LINE ||
+           (ctx->opt.line_from_level >= 0 && l >= ctx->opt.line_from_level);
+}
+bool fused_level(const wd_ctx* ctx, int l) {
+    return ctx->opt.smoother == WD_SMOOTH_FUSED && !line_level(ctx, l);
+}
 
 // one smoothing sweep on level l.
 //  * fused: lam -> lam2 in one launch, then the two buffers swap roles (the
@@ -893,7 +898,7 @@ int smooth_first_res(wd_ctx* ctx, bool prof, cudaStream_t st) {
 
 // can wd_solve take its convergence test from the first sweep of each cycle?
 bool lagged_residual(const wd_ctx* ctx) {
-    return ctx->opt.smoother == WD_SMOOTH_FUSED && ctx->nlev > 1 && ctx->opt.pre_smooth >= 1;
+    return fused_level(ctx, 0) && ctx->nlev > 1 && ctx->opt.pre_smooth >= 1;
 }
 
 // first = 1: the first level-0 pre-smoothing sweep has already run
@@ -1179,6 +1184,7 @@ void wd_default_options(wd_options* o) {
     o->rank = 0;
     o->nranks = 1;
     o->smoother = WD_SMOOTH_FUSED;
+    o->line_from_level = -1;
 }
 
 const char* wd_last_error(void) { return g_err; }

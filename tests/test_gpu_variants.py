@@ -146,3 +146,36 @@ def test_diverged_guard(wd):
     lam, rep = wd.wd_solve(ctx, wd.wd_rhs(ctx, p.u0), rel_tol=1e-10)
     assert rep["converged"]
     ctx.close()
+
+
+@pytest.mark.parametrize("line_from", [1, 2])
+@pytest.mark.parametrize("grid", ["small", "ragged"])
+def test_per_level_smoother_parity(wd, grid, line_from):
+    """Per-level smoother (SURVEY 8(f) f1 "per-level decisions"): the fused
+    point GS on the levels below `line_from`, vertical line
+    relaxation (reading C19) from it on -- GPU and oracle with the same
+    choice: hierarchy, one V-cycle <= 1e-10, the solve to 1e-10 (cycles +-1,
+    rate within 10 %, lambda <= 1e-8), bitwise-equal re-solve."""
+    p = synth.small() if grid == "small" else GRIDS["ragged"]()
+    X, Y, Z, u0 = p.numpy()
+    g = p.to(DEV)
+    cmax = 4096 if grid == "small" else 60
+    ctx = wd.wd_assemble(g.X, g.Y, g.Z, p.a, wd.default_options(coarsest_max_free=cmax,
+                                                                 line_from_level=line_from))
+    mg = oracle.MG(X, Y, Z, p.a, coarsest_max_free=cmax, line_from_level=line_from)
+    assert [ctx.level_dims(l) for l in range(ctx.num_levels())] == mg.dims
+    f_o = oracle.rhs(X, Y, Z, u0)
+    f = wd.wd_rhs(ctx, g.u0)
+    lam0 = synth.random_lambda(p, 4).numpy()
+    v = torch.as_tensor(lam0, device=DEV).clone()
+    wd.wd_vcycle(ctx, v, f, want_residual=False)
+    vo = mg.vcycle(lam0, f_o)
+    assert np.abs(_n(v) - vo).max() <= 1e-10 * np.abs(vo).max()
+    lam, rep = wd.wd_solve(ctx, f, rel_tol=1e-10)
+    lo, ro = mg.solve(f_o, tol=1e-10, max_cycles=100)
+    assert ro["status"] == 0 and abs(rep["cycles"] - ro["cycles"]) <= 1
+    assert abs(rep["rate"] - ro["rate"]) <= 0.1 * ro["rate"]
+    assert np.linalg.norm(_n(lam) - lo) <= 1e-8 * np.linalg.norm(lo)
+    lam2, _ = wd.wd_solve(ctx, f, rel_tol=1e-10)
+    assert torch.equal(lam, lam2)
+    ctx.close()
