@@ -123,7 +123,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 __global__ void __launch_bounds__(NTHR + 32, 1)
 apply_tma_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
                  const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mF,
-                 LevDev L, Tiles T, int with_f, int dbg, double* __restrict__ y,
+                 LevDev L, Tiles T, int with_f, int dbg, int jitter, double* __restrict__ y,
                  double* __restrict__ partial) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((128 - (sa(smem_raw) & 127)) & 127);
@@ -189,6 +189,13 @@ apply_tma_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__
     double xm[9], x0[9], xp[9];
 
     for (int s = 0; s < nsteps; s++) {
+        if (jitter) {   // race stress test (tests only, env WD_TEST_JITTER)
+            unsigned h = (unsigned)(blockIdx.x * 977u + warp * 131u + s * 7919u);
+            h ^= h >> 13;
+            h *= 0x5bd1e995u;
+            h ^= h >> 15;
+            __nanosleep(h % (unsigned)jitter);
+        }
         const int it = s / nk, k = s % nk;
         int a0, j0;
         tile_of(it, a0, j0);
@@ -367,9 +374,10 @@ int launch_apply_tma(const LevDev& L, const void* mapA, const void* mapB, const 
     if (g > T.ntiles) g = T.ntiles;
     const CUtensorMap* F = (const CUtensorMap*)(mapF ? mapF : mapX);
     g_launches += 1;
+    if (g_test_gs_grid > 0 && g > g_test_gs_grid) g = g_test_gs_grid;
     apply_tma_kernel<<<g, NTHR + 32, SMEM, st>>>(
         *(const CUtensorMap*)mapA, *(const CUtensorMap*)mapB, *(const CUtensorMap*)mapX, *F, L, T,
-        mapF ? 1 : 0, g_tma_debug, y, partial);
+        mapF ? 1 : 0, g_tma_debug, g_test_jitter, y, partial);
     return g;
 }
 

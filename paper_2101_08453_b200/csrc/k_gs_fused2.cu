@@ -112,7 +112,7 @@ template <bool RES>
 __global__ void __launch_bounds__(THREADS, 1)
 gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__ KBase KB,
                  LevDev L, double* __restrict__ lout, const double* __restrict__ f, int jt0,
-                 int ntx, int ntiles, double* __restrict__ partial) {
+                 int ntx, int ntiles, int jitter, double* __restrict__ partial) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* ring = reinterpret_cast<double*>(smem_raw + ((128 - (sa(smem_raw) & 127)) & 127));
     double* shadow = ring + PL * RING;
@@ -212,6 +212,17 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
         // the newest plane any colour reads at this step is s + 1 (colour 0)
         if (s + 1 < G) mbar_wait(&full[(s + 1) % RING], ((s + 1) / RING) & 1);
         if (s == 0 && G > 0) mbar_wait(&full[0], 0);
+        if (jitter) {
+            // race stress test (tests only, env WD_TEST_JITTER): every warp
+            // sleeps a pseudo-random 0..jitter ns before its step, so the warps
+            // and CTAs reach their reads and writes in shuffled orders; the
+            // result must not change (bitwise)
+            unsigned h = (unsigned)(blockIdx.x * 977u + (threadIdx.x >> 5) * 131u + s * 7919u);
+            h ^= h >> 13;
+            h *= 0x5bd1e995u;
+            h ^= h >> 15;
+            __nanosleep(h % (unsigned)jitter);
+        }
         const int g = s - LAG * c;
         if (g >= 0 && g < G) {
             const int z = zn;
@@ -357,14 +368,17 @@ int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map, 
     const int jt0 = L.own0 - ((L.own0 + L.jg0) & 1);
     const int ntx = (L.n1 + TI - 1) / TI, nty = (L.own1 - jt0 + TJ - 1) / TJ;
     g_launches += 1;
-    const int grid = std::min(ntx * nty, nsm);
+    // persistent CTAs; tests may cap their number (env WD_TEST_GS_GRID) so that
+    // other tiles share a CTA's cross-tile pipeline
+    int grid = std::min(ntx * nty, nsm);
+    if (g_test_gs_grid > 0) grid = std::min(grid, g_test_gs_grid);
     const CUtensorMap* m = (const CUtensorMap*)ring_map;
     if (partial)
         gs_fused2_kernel<true><<<grid, THREADS, SMEM_RES, st>>>(*m, KB, L, lout, f, jt0, ntx,
-                                                                ntx * nty, partial);
+                                                                ntx * nty, g_test_jitter, partial);
     else
         gs_fused2_kernel<false><<<grid, THREADS, SMEM, st>>>(*m, KB, L, lout, f, jt0, ntx,
-                                                             ntx * nty, nullptr);
+                                                             ntx * nty, g_test_jitter, nullptr);
     return grid;
 }
 

@@ -273,6 +273,7 @@ struct wd_ctx {
 namespace wd {
 std::atomic<long long> g_launches{0};
 int g_gs_v2 = 1;
+int g_test_jitter = 0, g_test_gs_grid = 0;
 int g_apply_variant = 1;
 int g_galerkin_generic = 0;
 }
@@ -1675,6 +1676,8 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
     if (const char* v = getenv("WD_TMA_DEBUG")) g_tma_debug = atoi(v);
     g_galerkin_generic = getenv("WD_GALERKIN_GENERIC") ? atoi(getenv("WD_GALERKIN_GENERIC")) : 0;
     g_gs_v2 = getenv("WD_GS_V2") ? atoi(getenv("WD_GS_V2")) : 1;
+    g_test_jitter = getenv("WD_TEST_JITTER") ? atoi(getenv("WD_TEST_JITTER")) : 0;
+    g_test_gs_grid = getenv("WD_TEST_GS_GRID") ? atoi(getenv("WD_TEST_GS_GRID")) : 0;
     if (!X || !Y || !Z) return fail(WD_E_INVAL, "NULL coordinate array");
     if (n1 < 3 || n2 < 3 || n3 < 2) return fail(WD_E_INVAL, "dims (%d,%d,%d): need n1,n2 >= 3, n3 >= 2", n1, n2, n3);
     if (n3 - 1 >= MAXNZ) return fail(WD_E_INVAL, "n3 = %d exceeds %d", n3, MAXNZ);

@@ -25,6 +25,10 @@ extern std::atomic<long long> g_launches;
 // development knob: thread mapping of apply_kernel (env WD_APPLY_VARIANT)
 extern int g_apply_variant;
 extern int g_tma_debug;
+// race stress tests (env WD_TEST_JITTER: max ns of a random per-warp sleep per
+// pipeline step in the fused sweep and the TMA residual; WD_TEST_GS_GRID: cap
+// on their persistent CTA count); 0 = off
+extern int g_test_jitter, g_test_gs_grid;
 extern int g_galerkin_generic;   // env WD_GALERKIN_GENERIC=1: disable the unrolled path (tests)
 
 typedef long long i64;

@@ -1,0 +1,87 @@
+"""Race stress tests of the pipelined kernels (compute-sanitizer's racecheck /
+synccheck are closed on this GPU pool -- running them has left GPUs needing a
+reset -- so the shared-memory rings, mbarrier pipelines and the cross-tile
+k-pipeline are exercised here by perturbing their timing instead).
+
+Test-only knobs (read at wd_assemble): WD_TEST_JITTER = n makes every warp of
+the fused sweep (k_gs_fused2.cu) and of the TMA residual (k_apply_tma.cu) sleep
+a pseudo-random 0..n ns before each pipeline step, so warps and CTAs reach
+their shared-memory reads / writes and barrier arrivals in shuffled orders;
+WD_TEST_GS_GRID = m caps their persistent CTA count at m, so the tiles pair up
+differently in each CTA's cross-tile pipeline.  A missing barrier, a ring
+slot reused too early or a halo read racing a neighbour's write would change
+the result; the bar is bitwise equality with the unperturbed run and with the
+phased four-launch schedule, which has no intra-kernel ordering
+to get wrong.
+"""
+import os
+
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+GRIDS = {
+    "ragged": lambda: synth.hill(nx=37, ny=22, nz=5, dx=40.0, height=120.0, sigma=300.0,
+                                 dz0=8.0, r=1.3, a=(1, 1, 3), device=DEV),
+    "small": lambda: synth.small(device=DEV),
+    "crop": lambda: synth.crop(synth.hill(nx=300, ny=200, nz=12, dx=30.0, height=250.0,
+                                          sigma=900.0, dz0=8.0, r=1.2, a=(1, 1, 10)),
+                               0, 0, 300, 200).to(DEV),
+}
+PERTURB = [(0, 0), (3000, 0), (0, 1), (0, 7), (2000, 5)]
+
+
+@pytest.fixture(scope="module")
+def wd():
+    import paper_2101_08453_b200 as m
+    return m
+
+
+def _ctx(wd, p, jitter=0, grid=0, **kw):
+    env = {"WD_TEST_JITTER": str(jitter), "WD_TEST_GS_GRID": str(grid)}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return wd.wd_assemble(p.X, p.Y, p.Z, p.a, wd.default_options(coarsest_max_free=60, **kw))
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("grid", list(GRIDS))
+def test_sweep_and_residual_under_perturbation(wd, grid):
+    p = GRIDS[grid]()
+    x0 = synth.random_lambda(p, 9)
+    ref_ctx = _ctx(wd, p, smoother="phased")
+    f = wd.wd_rhs(ref_ctx, p.u0)
+    ref = wd.wd_smooth(ref_ctx, 0, x0.clone(), f, sweeps=2)
+    ref_apply = wd.wd_apply(ref_ctx, 0, x0)
+    ref_ctx.close()
+    base = None
+    for jitter, cap in PERTURB:
+        ctx = _ctx(wd, p, jitter, cap)
+        got = wd.wd_smooth(ctx, 0, x0.clone(), f, sweeps=2)
+        assert torch.equal(got, ref), (jitter, cap)
+        assert torch.equal(wd.wd_apply(ctx, 0, x0), ref_apply), (jitter, cap)
+        lam, rep = wd.wd_solve(ctx, f, rel_tol=1e-9)   # residual-variant sweeps, graphs
+        torch.cuda.synchronize()
+        if base is None:
+            base = (lam, rep)
+        else:
+            assert torch.equal(lam, base[0]), (jitter, cap)
+            assert rep["cycles"] == base[1]["cycles"]
+            for a, b in zip(rep["hist"], base[1]["hist"]):
+                # per-CTA partial sums regroup when the CTA count changes
+                assert abs(a - b) <= 1e-12 * b, (jitter, cap)
+            if cap == 0:
+                assert rep["hist"] == base[1]["hist"]
+        ctx.close()
+    # knobs off again for later tests in this process
+    _ctx(wd, p).close()
