@@ -42,7 +42,7 @@ CONFIG_NAMES = {"tiny": "tiny 16x16x8 (configs[0])", "small": "small 128x128x10 
 # algorithmic HBM bytes per free node of one launch of the level-0 smoother:
 #   fused sweep (1 launch/sweep): 14 stored couplings (112) + f (8) + lambda read + write (16)
 #   colour phase (4 launches/sweep, --smoother phased): 264 B/node/sweep / 4
-GS_BYTES = {"fused": (136, 1, "gs_fused_kernel"), "phased": (66, 4, "gs_phase_kernel")}
+GS_BYTES = {"fused": (136, 1, "gs_fused2_kernel"), "phased": (66, 4, "gs_phase_kernel")}
 CPU_CROP = 200                            # oracle sample: 200x200x15 elements of the workload
 
 
@@ -371,13 +371,20 @@ def run_ours(args, ws, rank, local):
     achieved = bytes_launch / (launch_ms * 1e-3) / 1e9 if launch_ms > 0 else 0.0
     plain_ms = gs_ms / max(gs_sweeps, 1) / gs_per_sweep
     res_ms = gsr_ms / max(gsr_sweeps, 1) if gsr_sweeps else None
-    traffic = None
+    traffic, traffic_res = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_gs_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(f"{gs_name}:{args.config}")
+            tj = json.load(open(tp))
+            traffic = tj.get(f"{gs_name}:{args.config}")
+            traffic_res = tj.get(f"{gs_name}_res:{args.config}")
         except Exception:
             traffic = None
+    if traffic is not None and traffic_res is not None and n_all:
+        # per launch, weighted like `achieved` (plain and residual-variant launches)
+        traffic_all = (traffic * gs_sweeps + traffic_res * gsr_sweeps) / n_all
+    else:
+        traffic_all = traffic
 
     line = None
     if rank == 0:
@@ -405,13 +412,15 @@ def run_ours(args, ws, rank, local):
             "roofline": {"kernel": f"{gs_name} (level 0, all sweeps incl. the residual "
                                    "variant, time-weighted)", "bound": "hbm",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic_all,
                          "bytes_per_launch": bytes_launch, "launch_ms": launch_ms,
                          "launches": n_all * gs_per_sweep,
                          "plain": {"launch_ms": plain_ms, "launches": gs_sweeps * gs_per_sweep,
+                                   "traffic": traffic,
                                    "frac": (bytes_launch / (plain_ms * 1e-3) / 1e9 / peak
                                             if plain_ms > 0 else None)},
                          "residual_variant": {"launch_ms": res_ms, "launches": gsr_sweeps,
+                                              "traffic": traffic_res,
                                               "frac": (bytes_launch / (res_ms * 1e-3) / 1e9 / peak
                                                        if res_ms else None)},
                          "peak_source": peak_src},

@@ -21,6 +21,8 @@
 
 #include "wd_internal.cuh"
 
+#include <cstdlib>
+
 namespace wd {
 
 int g_tma_debug = 0;   // development knob (env WD_TMA_DEBUG): bit mask of disabled TMA rings
@@ -294,6 +296,17 @@ apply_tma_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__
     }
 }
 
+// L2 promotion of the residual's TMA boxes (env WD_APPLY_L2PROMO 0..3 = none,
+// 64, 128, 256 B; default 256 B)
+CUtensorMapL2promotion apply_promo() {
+    static const CUtensorMapL2promotion promo[4] = {
+        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+    int pr = 3;
+    if (const char* e = getenv("WD_APPLY_L2PROMO")) pr = atoi(e) & 3;
+    return promo[pr];
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -331,10 +344,10 @@ int make_coef_maps(const LevDev& L, const double* coef, void* mapA, void* mapB) 
     cuuint32_t boxB[5] = {BP, 2, B_ROWS, 1, 9};
     CUresult r1 = enc((CUtensorMap*)mapA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)coef, dims,
                       str, boxA, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      apply_promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     CUresult r2 = enc((CUtensorMap*)mapB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)coef, dims,
                       str, boxB, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      apply_promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return (r1 == CUDA_SUCCESS && r2 == CUDA_SUCCESS) ? 0 : -1;
 }
 
@@ -352,7 +365,7 @@ int make_vec_map(const LevDev& L, const double* v, void* map, bool halo) {
     cuuint32_t boxF[4] = {TI, 2, TJ, 1};
     CUresult r = enc((CUtensorMap*)map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)v, dims, str,
                      halo ? boxX : boxF, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, apply_promo(),
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : -1;
 }

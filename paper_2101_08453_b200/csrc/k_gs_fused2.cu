@@ -32,6 +32,7 @@
 #include "wd_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 
 namespace wd {
@@ -331,9 +332,14 @@ int make_ring_map(const LevDev& L, const double* v, void* map) {
     cuuint64_t str[3] = {(cuuint64_t)L.H * 8, (cuuint64_t)L.sk * 8, (cuuint64_t)L.sj * 8};
     cuuint32_t es[4] = {1, 1, 1, 1};
     cuuint32_t box[4] = {SW, 2, 1, SH};
+    static const CUtensorMapL2promotion promo[4] = {
+        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+    int pr = 0;
+    if (const char* e = getenv("WD_RING_L2PROMO")) pr = atoi(e) & 3;
     CUresult r = enc((CUtensorMap*)map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)v, dims, str,
-                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo[pr],
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : -1;
 }
 

@@ -38,26 +38,41 @@ def launches(path, out):
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr = rows[hi]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    mi = hdr.index("Metric Name")
     tot, cnt = collections.defaultdict(float), collections.Counter()
+    dram = collections.defaultdict(float)
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
-        v = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1.0)
         name = r[ki].split("(")[0].replace("wd::<unnamed>::", "").replace(
             "wd::(anonymous namespace)::", "")
         if name.startswith("void at::") or name.startswith("at::"):
             name = "[torch input generation / bench glue]"
-        tot[name] += v
-        cnt[name] += 1
-    T = sum(tot.values())
+        v = float(r[vi].replace(",", ""))
+        if r[mi] == "gpu__time_duration.sum":
+            tot[name] += v * SCALE.get(r[ui], 1.0)
+            cnt[name] += 1
+        elif r[mi].startswith("dram__bytes_"):
+            dram[name] += v * SCALE.get(r[ui], 1.0)
     own = sum(v for k, v in tot.items() if not k.startswith("["))
-    lines = [f"# per-kernel device time from {os.path.basename(path)} (ncu gpu__time_duration.sum,"
-             " --clock-control none; cold-cache serialised launches: compare SHARES)",
-             f"{'kernel':44s} {'launches':>8s} {'total ms':>10s} {'% of wd':>8s}"]
+    has_dram = bool(dram)
+    lines = [f"# per-kernel device time from {os.path.basename(path)} (ncu gpu__time_duration.sum"
+             + (", dram__bytes_read/write.sum" if has_dram else "") +
+             ", --clock-control none; cold-cache serialised launches: compare SHARES)",
+             f"{'kernel':44s} {'launches':>8s} {'total ms':>10s} {'% of wd':>8s}"
+             + (f" {'GB':>9s} {'TB/s':>6s}" if has_dram else "")]
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         share = f"{100 * v / own:7.1f}%" if not k.startswith("[") else "     -  "
-        lines.append(f"{k:44s} {cnt[k]:8d} {v:10.3f} {share}")
-    lines.append(f"{'total wd kernels':44s} {'':8s} {own:10.3f}")
+        ln = f"{k:44s} {cnt[k]:8d} {v:10.3f} {share}"
+        if has_dram:
+            gb = dram[k] / 1e9
+            ln += f" {gb:9.2f} {gb / v if v > 0 else 0:6.2f}"
+        lines.append(ln)
+    ln = f"{'total wd kernels':44s} {'':8s} {own:10.3f}"
+    if has_dram:
+        gb = sum(v for k, v in dram.items() if not k.startswith("[")) / 1e9
+        ln += f" {'':8s} {gb:9.2f} {gb / own:6.2f}"
+    lines.append(ln)
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
