@@ -181,8 +181,15 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
         if (++zl == n3) { zl = 0; ++kl; }
     };
     __syncthreads();   // ring zeroed, barriers initialised
-    if (threadIdx.x == 0)
+    // One thread issues the plane loads and waits for their mbarriers; the
+    // CTA barrier that follows its wait orders the landed plane before every
+    // other thread's reads (the waiting thread acquires the TMA writes, the
+    // barrier carries them on), so the 608 threads do not poll the mbarriers.
+    if (threadIdx.x == 0) {
         for (int p = 0; p < LA && p < G; p++) issue();
+        for (int p = 0; p < 2 && p < G; p++) mbar_wait(&full[p], 0);
+    }
+    __syncthreads();
 
     double kf[13], kb[13], fv = 0.0, kd = 1.0;
     auto load_k = [&](int z) {
@@ -210,9 +217,6 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
     const int nsteps = G + LAG * 3;
     for (int s = 0; s < nsteps; s++) {
         if (threadIdx.x == 0 && s + LA < G) issue();
-        // the newest plane any colour reads at this step is s + 1 (colour 0)
-        if (s + 1 < G) mbar_wait(&full[(s + 1) % RING], ((s + 1) / RING) & 1);
-        if (s == 0 && G > 0) mbar_wait(&full[0], 0);
         if (jitter) {
             // race stress test (tests only, env WD_TEST_JITTER): every warp
             // sleeps a pseudo-random 0..jitter ns before its step, so the warps
@@ -291,6 +295,8 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
         } else if (g == -1 && act && G > 0) {
             load_k(0);
         }
+        // the newest plane read at step s + 1 is s + 2 (colour 0's plane above)
+        if (threadIdx.x == 0 && s + 2 < G) mbar_wait(&full[(s + 2) % RING], ((s + 2) / RING) & 1);
         __syncthreads();
     }
     if (RES) {
