@@ -55,7 +55,8 @@ constexpr unsigned BOX_BYTES = PLD * 8;
 constexpr int B0 = TJ / 2 + 1, B1 = TJ / 2 + 1, B2 = TJ / 2, B3 = TJ / 2;
 constexpr int W0 = B0, W1 = W0 + B1, W2 = W1 + B2, W3 = W2 + B3;   // warp ranges
 constexpr int NHALO = 3 * B0 + 2 * B1 + B2;                          // 29 halo columns
-constexpr int THREADS = 32 * (W3 + 1);                               // 19 warps
+constexpr int PRODUCER = 32 * (W3 + 1);                              // first thread of the TMA warp
+constexpr int THREADS = 32 * (W3 + 2);   // 18 colour warps, 1 halo warp, 1 TMA producer warp
 constexpr int SHADOW = 8;
 constexpr size_t SMEM = sizeof(double) * PL * RING + 8 * RING + 128;
 constexpr size_t SMEM_RES = SMEM + sizeof(double) * PL * SHADOW;
@@ -131,6 +132,7 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
     else if (w < W1) { c = 1; dj = 2 * (w - W0); di = 1 + 2 * lane; }
     else if (w < W2) { c = 2; dj = 1 + 2 * (w - W1); di = 2 * lane; }
     else if (w < W3) { c = 3; dj = 1 + 2 * (w - W2); di = 1 + 2 * lane; }
+    else if (w > W3) { c = 0; dj = 0; di = -10; inreg = false; }   // the TMA producer warp
     else if (lane < 3 * B0) {
         c = 0; dj = 2 * (lane / 3);
         const int e = lane % 3;
@@ -185,7 +187,7 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
     // CTA barrier that follows its wait orders the landed plane before every
     // other thread's reads (the waiting thread acquires the TMA writes, the
     // barrier carries them on), so the 608 threads do not poll the mbarriers.
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == PRODUCER) {
         for (int p = 0; p < LA && p < G; p++) issue();
         for (int p = 0; p < 2 && p < G; p++) mbar_wait(&full[p], 0);
     }
@@ -216,7 +218,7 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
     double rr = 0.0;
     const int nsteps = G + LAG * 3;
     for (int s = 0; s < nsteps; s++) {
-        if (threadIdx.x == 0 && s + LA < G) issue();
+        if (threadIdx.x == PRODUCER && s + LA < G) issue();
         if (jitter) {
             // race stress test (tests only, env WD_TEST_JITTER): every warp
             // sleeps a pseudo-random 0..jitter ns before its step, so the warps
@@ -296,7 +298,8 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
             load_k(0);
         }
         // the newest plane read at step s + 1 is s + 2 (colour 0's plane above)
-        if (threadIdx.x == 0 && s + 2 < G) mbar_wait(&full[(s + 2) % RING], ((s + 2) / RING) & 1);
+        if (threadIdx.x == PRODUCER && s + 2 < G)
+            mbar_wait(&full[(s + 2) % RING], ((s + 2) / RING) & 1);
         __syncthreads();
     }
     if (RES) {
