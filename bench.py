@@ -43,7 +43,7 @@ CONFIG_NAMES = {"tiny": "tiny 16x16x8 (configs[0])", "small": "small 128x128x10 
 #   fused sweep (1 launch/sweep): 14 stored couplings (112) + f (8) + lambda read + write (16)
 #   colour phase (4 launches/sweep, --smoother phased): 264 B/node/sweep / 4
 GS_BYTES = {"fused": (136, 1, "gs_fused2_kernel"), "phased": (66, 4, "gs_phase_kernel")}
-CPU_CROP = 200                            # oracle sample: 200x200x15 elements of the workload
+CPU_CROP = 500                            # oracle sample: 500x500x15 elements of the workload
 
 
 def vcycle_hbm(levels, ms, peak, sweeps=4):
@@ -532,7 +532,7 @@ def run_ours(args, ws, rank, local):
         import oracle
         samp = cpu_sample(prob)
         tot, cyc, nst = 0.0, 0, 0
-        while tot < 10.0 and nst < 4:
+        while tot < 10.0 and nst < 20:   # ~10-30 s of oracle work
             dt, c, _ = oracle_step(samp, args.tol)
             tot += dt
             cyc += c
