@@ -44,25 +44,29 @@ __global__ void dense_build_kernel(LevDev L, const double* __restrict__ K, doubl
             }
 }
 
-// (1) invert the diagonal block in shared memory (scalar Gauss-Jordan)
+// (1) invert the diagonal block in shared memory (scalar Gauss-Jordan,
+//     double-buffered: one barrier per pivot, one division per pivot)
 __global__ void gj_diag_kernel(const double* __restrict__ A, int n, int k0, int nb, double* Dinv) {
-    __shared__ double D[BS][BS + 1];
+    __shared__ double D[2][BS][BS + 1];
     const int r = threadIdx.y, c = threadIdx.x;
-    D[r][c] = (r < nb && c < nb) ? A[(i64)(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
+    D[0][r][c] = (r < nb && c < nb) ? A[(i64)(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
     __syncthreads();
+    int b = 0;
     for (int t = 0; t < BS; t++) {
-        const double piv = D[t][t];
-        const double drt = D[r][t], dtc = D[t][c], drc = D[r][c];
-        __syncthreads();
+        const double (&S)[BS][BS + 1] = D[b];
+        const double piv = S[t][t];
+        const double ip = 1.0 / piv;   // every thread, same value (no extra barrier)
+        const double drt = S[r][t], dtc = S[t][c], drc = S[r][c];
         double v;
-        if (r == t && c == t) v = 1.0 / piv;
-        else if (r == t) v = dtc / piv;
-        else if (c == t) v = -drt / piv;
-        else v = drc - drt * (dtc / piv);
-        D[r][c] = v;
+        if (r == t && c == t) v = ip;
+        else if (r == t) v = dtc * ip;
+        else if (c == t) v = -drt * ip;
+        else v = drc - drt * (dtc * ip);
+        D[b ^ 1][r][c] = v;
+        b ^= 1;
         __syncthreads();
     }
-    Dinv[r * BS + c] = D[r][c];
+    Dinv[r * BS + c] = D[b][r][c];
 }
 
 // (2) row panel: A_Kj <- Dinv A_Kj  (j outside block K)
@@ -82,21 +86,51 @@ __global__ void gj_row_kernel(double* A, int n, int k0, int nb, const double* __
     }
 }
 
-// (3) trailing update: A_ij -= A_iK A_Kj(new), i, j outside block K
-__global__ void gj_trail_kernel(double* A, int n, int k0, int nb) {
-    const int kb = k0 / BS;
-    if ((int)blockIdx.x == kb || (int)blockIdx.y == kb) return;
-    __shared__ double Ac[BS][BS + 1], Ar[BS][BS + 1];
-    const int r = threadIdx.y, c = threadIdx.x;
-    const int i = blockIdx.y * BS + r, j = blockIdx.x * BS + c;
-    const int ir = blockIdx.y * BS + r;   // row of Ac tile
-    Ac[r][c] = (ir < n && c < nb) ? A[(i64)ir * n + k0 + c] : 0.0;
-    Ar[r][c] = (r < nb && j < n) ? A[(i64)(k0 + r) * n + j] : 0.0;
+// (3) trailing update: A_ij -= A_iK A_Kj(new), i, j outside block K.
+//     64 x 64 output tiles, 256 threads with 4 x 4 outputs each (register
+//     tiling), the K-panel (<= 32 wide) staged in shared memory
+constexpr int TT = 64;
+__global__ void __launch_bounds__(256)
+gj_trail_kernel(double* A, int n, int k0, int nb) {
+    __shared__ double Ac[TT][BS + 1], Ar[BS][TT + 1];
+    const int tid = threadIdx.x;
+    const int i0 = blockIdx.y * TT, j0 = blockIdx.x * TT;
+    for (int e = tid; e < TT * BS; e += 256) {
+        const int rr = e / BS, cc = e % BS;
+        const int i = i0 + rr;
+        Ac[rr][cc] = (i < n && cc < nb && (i < k0 || i >= k0 + nb)) ? A[(i64)i * n + k0 + cc] : 0.0;
+        const int r2 = e / TT, c2 = e % TT;
+        const int j = j0 + c2;
+        Ar[r2][c2] = (r2 < nb && j < n) ? A[(i64)(k0 + r2) * n + j] : 0.0;
+    }
     __syncthreads();
-    if (i < n && j < n) {
-        double s = A[(i64)i * n + j];
-        for (int t = 0; t < nb; t++) s = fma(-Ac[r][t], Ar[t][c], s);
-        A[(i64)i * n + j] = s;
+    const int ty = tid / 16, tx = tid % 16;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) acc[a][b] = 0.0;
+    for (int t = 0; t < nb; t++) {
+        double x[4], y[4];
+#pragma unroll
+        for (int a = 0; a < 4; a++) x[a] = Ac[ty + 16 * a][t];
+#pragma unroll
+        for (int b = 0; b < 4; b++) y[b] = Ar[t][tx + 16 * b];
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+            for (int b = 0; b < 4; b++) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+        const int i = i0 + ty + 16 * a;
+        if (i >= n || (i >= k0 && i < k0 + nb)) continue;
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int j = j0 + tx + 16 * b;
+            if (j >= n || (j >= k0 && j < k0 + nb)) continue;
+            A[(i64)i * n + j] -= acc[a][b];
+        }
     }
 }
 
@@ -171,7 +205,8 @@ int gj_invert(double* A, int n, double* Dinv, cudaStream_t st) {
         g_launches += 4;
         gj_diag_kernel<<<1, blk, 0, st>>>(A, n, k0, nb, Dinv);
         gj_row_kernel<<<nbk, blk, 0, st>>>(A, n, k0, nb, Dinv);
-        gj_trail_kernel<<<dim3(nbk, nbk), blk, 0, st>>>(A, n, k0, nb);
+        const int ntt = (n + TT - 1) / TT;
+        gj_trail_kernel<<<dim3(ntt, ntt), 256, 0, st>>>(A, n, k0, nb);
         gj_col_kernel<<<nbk, blk, 0, st>>>(A, n, k0, nb, Dinv);
     }
     return 0;
