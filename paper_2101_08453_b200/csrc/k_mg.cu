@@ -116,12 +116,16 @@ gs_phase_kernel(LevDev L, const double* __restrict__ K, double* lam,
 // neighbours, so the phase is order-independent):  T x = f - (off-column
 // part of K x), T tridiagonal with a_k = K(k, k-1) (slot 9 stored at k-1),
 // b_k = K(k, k), c_k = K(k, k+1) (slot 9 at k; the top plane is Dirichlet).
-// Thomas algorithm: forward elimination bottom-up (c'_k into cpb, d'_k into
-// dpb at the node's own offset), back substitution top-down into lam.
+// Thomas algorithm: forward elimination bottom-up, back substitution top-down
+// into lam.  c'_k, d'_k are kept in shared memory ([k][thread], conflict
+// free) when the column fits (SMEM_T), else in the two scratch arrays cpb,
+// dpb at the node's own offset (HBM).
+template <bool SMEM_T>
 __global__ void __launch_bounds__(GS_BLK)
 line_phase_kernel(LevDev L, const double* __restrict__ K, double* lam,
                   const double* __restrict__ f, double* __restrict__ cpb, double* __restrict__ dpb,
                   int ci, int cj) {
+    extern __shared__ double tsc[];   // SMEM_T: c' at [k][t], d' at [m + k][t]
     const int a = blockIdx.x * GS_BLK + threadIdx.x;
     const int i = 2 * a + ci;
     const int j = L.own0 + ((cj - (L.own0 + L.jg0)) & 1) + 2 * (int)blockIdx.y;
@@ -173,8 +177,13 @@ line_phase_kernel(LevDev L, const double* __restrict__ K, double* lam,
             cp = cc / mk;
             dp = (r - ak * dprev) / mk;
         }
-        cpb[base] = cp;
-        dpb[base] = dp;
+        if (SMEM_T) {
+            tsc[k * GS_BLK + threadIdx.x] = cp;
+            tsc[(m + k) * GS_BLK + threadIdx.x] = dp;
+        } else {
+            cpb[base] = cp;
+            dpb[base] = dp;
+        }
         cprev = cp;
         dprev = dp;
 #pragma unroll
@@ -193,7 +202,10 @@ line_phase_kernel(LevDev L, const double* __restrict__ K, double* lam,
     lam[own + (i64)(m - 1) * L.sk] = xn;
     for (int k = m - 2; k >= 0; k--) {
         const i64 base = own + (i64)k * L.sk;
-        xn = dpb[base] - cpb[base] * xn;
+        if (SMEM_T)
+            xn = tsc[(m + k) * GS_BLK + threadIdx.x] - tsc[k * GS_BLK + threadIdx.x] * xn;
+        else
+            xn = dpb[base] - cpb[base] * xn;
         lam[base] = xn;
     }
 }
@@ -711,7 +723,25 @@ void launch_line_phase(const LevDev& L, const double* coef, double* lam, const d
     const int half = (L.n1 + 1) / 2;
     dim3 grid((half + GS_BLK - 1) / GS_BLK, (L.own1 - L.own0 + 2) / 2);
     g_launches += 1;
-    line_phase_kernel<<<grid, GS_BLK, 0, st>>>(L, coef, lam, f, cpb, dpb, colour[c][0], colour[c][1]);
+    // the Thomas scratch of a column in shared memory when it fits (n3 <= 33:
+    // <= 64 KB per 128-thread block), else in HBM
+    const int m = L.n3 - 1;
+    const size_t smem = sizeof(double) * 2 * (size_t)m * GS_BLK;
+    if (m <= 32) {
+        static int attr_set[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+            cudaFuncSetAttribute(line_phase_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 64 * 1024 + 1024);
+            attr_set[dev] = 1;
+        }
+        line_phase_kernel<true><<<grid, GS_BLK, smem, st>>>(L, coef, lam, f, cpb, dpb, colour[c][0],
+                                                            colour[c][1]);
+    } else {
+        line_phase_kernel<false><<<grid, GS_BLK, 0, st>>>(L, coef, lam, f, cpb, dpb, colour[c][0],
+                                                          colour[c][1]);
+    }
 }
 
 void launch_gs_sweep(const LevDev& L, const double* coef, double* lam, const double* f,
