@@ -21,9 +21,16 @@
  * contraction) so every line below is evaluated as written.
  *
  * Parity status of each function: see DESIGN.md "Oracle pins".  Every
- * function here is pinned by tests/test_oracle_*.py except the V-cycle
- * convergence factor, which is pinned only by the paper's anchors
- * -- "parity unpinned" beyond those anchors.
+ * function here is pinned by tests/test_oracle_*.py.  The V-cycle and its
+ * convergence factor are pinned against a dense recursive V-cycle on 3-4
+ * level hierarchies (tests/test_oracle_vcycle_dense.py); at large sizes the
+ * factor rests on the same code plus the paper's anchors (P:169-172,
+ * P:200-202).
+ *
+ * The scatter loops run owner-partitioned under OpenMP (own_rows): each
+ * thread performs the serial loop in the serial order and adds only into the
+ * target rows it owns, so the result is bitwise that of one thread
+ * (tests/test_oracle_threads.py).
  */
 #include <math.h>
 #include <stdlib.h>
