@@ -64,6 +64,13 @@ def test_sweep_and_residual_under_perturbation(wd, grid):
     ref = wd.wd_smooth(ref_ctx, 0, x0.clone(), f, sweeps=2)
     ref_apply = wd.wd_apply(ref_ctx, 0, x0)
     ref_ctx.close()
+    try:
+        _perturbed_runs(wd, p, x0, f, ref, ref_apply)
+    finally:
+        _ctx(wd, p).close()   # knobs off again for later tests in this process
+
+
+def _perturbed_runs(wd, p, x0, f, ref, ref_apply):
     base = None
     for jitter, cap in PERTURB:
         ctx = _ctx(wd, p, jitter, cap)
@@ -83,5 +90,3 @@ def test_sweep_and_residual_under_perturbation(wd, grid):
             if cap == 0:
                 assert rep["hist"] == base[1]["hist"]
         ctx.close()
-    # knobs off again for later tests in this process
-    _ctx(wd, p).close()
