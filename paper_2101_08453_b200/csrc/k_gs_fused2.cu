@@ -60,6 +60,9 @@ constexpr int THREADS = 32 * (W3 + 2);   // 18 colour warps, 1 halo warp, 1 TMA 
 constexpr int SHADOW = 8;
 constexpr size_t SMEM = sizeof(double) * PL * RING + 8 * RING + 128;
 constexpr size_t SMEM_RES = SMEM + sizeof(double) * PL * SHADOW;
+constexpr int CXM = 40, CYM = 8, CPL = CXM * CYM;   // PRO: coarse region under a tile
+// PRO: two coarse planes + the x / y tables of the ring's columns and rows
+constexpr size_t SMEM_PRO = SMEM + sizeof(double) * 2 * CPL + sizeof(int) * (RW + SH + 16);
 static_assert(NHALO <= 32, "halo columns must fit one warp");
 static_assert(RING >= LA + 8, "ring too short");
 
@@ -102,6 +105,24 @@ __device__ __forceinline__ void tma4(void* dst, const CUtensorMap* m, int c0, in
         : "memory");
 }
 
+// Fused prolongation (PRO variant, the first post-smoothing sweep of a level
+// whose transition to the next level is horizontal with an identity z map):
+// the sweep's input is lambda + w P lambda_c (Eq. (7) "u <- u + P u_c",
+// P:176-181) formed in the ring as each plane lands, so the separate
+// prolongation pass (lambda read + write) disappears.  The producer warp
+// stages the coarse values under the tile (<= CXM x CYM per plane, one plane
+// ahead by cp.async) and corrects every free node of a landed ring plane with
+// exactly prolong_kernel's operations (bitwise equal to prolong + sweep).
+struct ProArgs {
+    const double* xc;         // coarse lambda (i-split layout of level C)
+    LevDev C;                 // the coarse level
+    const int* lox;           // fine index -> lower parent (x), coincident flag
+    const int* cox;
+    const int* loy;
+    const int* coy;
+    double w;                 // correction weight (1 = Eq. (7))
+};
+
 // base pointers of the coupling loads: slot s of node p is kf[s][o(p)];
 // the backward coupling K(p, p - d_s) = K_s[p - d_s] is kb[s][o(p) + x shift]
 // (kb[s] already holds the row / plane shift of -d_s)
@@ -110,16 +131,24 @@ struct KBase {
     const double* kb[14];
 };
 
-template <bool RES>
+// MODE 0: plain sweep; 1 (RES): also ||f - K lin||^2; 2 (PRO): input lin + w P xc
+template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
 gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__ KBase KB,
                  LevDev L, double* __restrict__ lout, const double* __restrict__ f, int jt0,
-                 int ntx, int ntiles, int jitter, double* __restrict__ partial) {
+                 int ntx, int ntiles, int jitter, double* __restrict__ partial,
+                 const __grid_constant__ ProArgs PA) {
+    constexpr bool RES = MODE == 1, PRO = MODE == 2;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* ring = reinterpret_cast<double*>(smem_raw + ((128 - (sa(smem_raw) & 127)) & 127));
     double* shadow = ring + PL * RING;
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + PL * (RING + (RES ? SHADOW : 0)));
-    for (int t = threadIdx.x; t < PL * (RING + (RES ? SHADOW : 0)); t += THREADS) ring[t] = 0.0;
+    double* csm = ring + PL * RING;                           // PRO: coarse planes [2][CPL]
+    int* xtab = reinterpret_cast<int*>(csm + 2 * CPL);          // PRO: per ring column (RW)
+    int* ytab = xtab + RW;                                      // PRO: per ring row (SH)
+    constexpr int EXTRA = RES ? PL * SHADOW : PRO ? 2 * CPL + (RW + SH + 16) / 2 : 0;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + PL * RING + EXTRA);
+    for (int t = threadIdx.x; t < PL * RING + (RES ? PL * SHADOW : PRO ? 2 * CPL : 0); t += THREADS)
+        ring[t] = 0.0;
     if (threadIdx.x == 0) {
         for (int t = 0; t < RING; t++) mbar_init(&full[t], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -182,6 +211,83 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
         if (++lslot == RING) lslot = 0;
         if (++zl == n3) { zl = 0; ++kl; }
     };
+    // PRO (producer warp, all 32 lanes): coarse region origin of a tile, the
+    // column / row tables, the staging of one coarse plane and the correction
+    const bool prow = PRO && w == W3 + 1;
+    int pcI0 = 0, pcJ0 = 0, ptile = -1;   // tile whose tables are in xtab / ytab
+    auto coarse_origin = [&](int tk, int& cI0, int& cJ0) {
+        int I0, J0;
+        origin(tk, I0, J0);
+        cI0 = __ldg(PA.lox + max(I0 - 4, 0));
+        cJ0 = __ldg(PA.loy + max(J0 - 1, 0));
+    };
+    auto stage_coarse = [&](int q) {   // plane q's coarse values -> csm[q & 1] (cp.async)
+        const int tk = q / n3, z = q - tk * n3;
+        int cI0, cJ0;
+        coarse_origin(tk, cI0, cJ0);
+        double* dst = csm + (q & 1) * CPL;
+        for (int e = lane; e < CPL; e += 32) {
+            const int I = cI0 + e % CXM, J = cJ0 + e / CXM;
+            if (I < PA.C.n1 && J < PA.C.n2 && z < PA.C.n3) {
+                const unsigned sd = (unsigned)__cvta_generic_to_shared(dst + e);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sd),
+                             "l"(PA.xc + loff(PA.C, I, J, z)) : "memory");
+            } else {
+                dst[e] = 0.0;
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    auto build_tables = [&](int tk) {   // ring column r / row rj -> packed parent info
+        int I0, J0;
+        origin(tk, I0, J0);
+        coarse_origin(tk, pcI0, pcJ0);
+        for (int r = lane; r < RW + SH; r += 32) {
+            if (r < RW) {   // column: half = r / SW, pos = r % SW
+                const int i = I0 - 4 + 2 * (r % SW) + r / SW;
+                int v = -1;
+                if (i >= 1 && i <= L.n1 - 2)
+                    v = ((__ldg(PA.lox + i) - pcI0) << 1) | (__ldg(PA.cox + i) ? 0 : 1);
+                xtab[r] = v;
+            } else {
+                const int rj = r - RW, j = J0 - 1 + rj;
+                int v = -1;
+                if (j >= 0 && j < L.n2 && row_free(L, j))
+                    v = ((__ldg(PA.loy + j) - pcJ0) << 1) | (__ldg(PA.coy + j) ? 0 : 1);
+                ytab[rj] = v;
+            }
+        }
+        ptile = tk;
+    };
+    // ring plane q (landed) += w P (coarse plane q), on its free nodes; same
+    // operations as prolong_kernel's identity-z path (bitwise equal)
+    auto correct_plane = [&](int q) {
+        const int tk = q / n3, z = q - tk * n3;
+        if (tk != ptile) build_tables(tk);
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+        if (z >= nz) return;
+        const double* cs = csm + (q & 1) * CPL;
+        double* rp = ring + (q % RING) * PL;
+        for (int e = lane; e < PLD; e += 32) {
+            const int rj = e / RW, r = e - rj * RW;
+            const int xt = xtab[r], yt = ytab[rj];
+            if (xt < 0 || yt < 0) continue;
+            const int ix = xt >> 1, iy = yt >> 1;
+            const bool two = xt & 1, ny2 = yt & 1;
+            const double wx = two ? 0.5 : 1.0, wy = ny2 ? 0.5 : 1.0;
+            const double* c0 = cs + iy * CXM + ix;
+            double sr = 0.0 + c0[0];
+            sr += two ? c0[1] : -0.0;
+            double sv = fma(wy * 1.0, wx * sr, 0.0);
+            if (ny2) {
+                double sr2 = 0.0 + c0[CXM];
+                sr2 += two ? c0[CXM + 1] : -0.0;
+                sv = fma(wy * 1.0, wx * sr2, sv);
+            }
+            rp[e] = fma(PA.w, sv, rp[e]);
+        }
+    };
     __syncthreads();   // ring zeroed, barriers initialised
     // One thread issues the plane loads and waits for their mbarriers; the
     // CTA barrier that follows its wait orders the landed plane before every
@@ -190,6 +296,14 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
     if (threadIdx.x == PRODUCER) {
         for (int p = 0; p < LA && p < G; p++) issue();
         for (int p = 0; p < 2 && p < G; p++) mbar_wait(&full[p], 0);
+    }
+    if (prow) {   // planes 0 and 1 corrected before the first step, plane 2 staged
+        __syncwarp();
+        for (int p = 0; p < 2 && p < G; p++) {
+            stage_coarse(p);
+            correct_plane(p);
+        }
+        if (2 < G) stage_coarse(2);
     }
     __syncthreads();
 
@@ -300,6 +414,11 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
         // the newest plane read at step s + 1 is s + 2 (colour 0's plane above)
         if (threadIdx.x == PRODUCER && s + 2 < G)
             mbar_wait(&full[(s + 2) % RING], ((s + 2) / RING) & 1);
+        if (prow && s + 2 < G) {   // correct plane s + 2, stage the coarse plane s + 3
+            __syncwarp();
+            correct_plane(s + 2);
+            if (s + 3 < G) stage_coarse(s + 3);
+        }
         __syncthreads();
     }
     if (RES) {
@@ -359,8 +478,9 @@ int gs_fused2_prepare() {
     if (dev < 0 || dev >= 64) dev = 0;
     int nsm = nsm_dev[dev].load(std::memory_order_acquire);
     if (nsm > 0) return nsm;
-    cudaFuncSetAttribute(gs_fused2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    cudaFuncSetAttribute(gs_fused2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RES);
+    cudaFuncSetAttribute(gs_fused2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(gs_fused2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RES);
+    cudaFuncSetAttribute(gs_fused2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_PRO);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
     nsm_dev[dev].store(nsm, std::memory_order_release);
@@ -370,7 +490,7 @@ int gs_fused2_prepare() {
 // one sweep lin -> lout (k_gs_fused.cu launch_gs_fused); ring_map: the
 // make_ring_map tensor map of lin
 int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map, double* lout,
-                     const double* f, cudaStream_t st, double* partial) {
+                     const double* f, cudaStream_t st, double* partial, const ProlongIn* pro) {
     const int nsm = gs_fused2_prepare();
     KBase KB;
     for (int s = 0; s < 14; s++) {
@@ -388,12 +508,25 @@ int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map, 
     int grid = std::min(ntx * nty, nsm);
     if (g_test_gs_grid > 0) grid = std::min(grid, g_test_gs_grid);
     const CUtensorMap* m = (const CUtensorMap*)ring_map;
+    ProArgs PA{};
+    if (pro) {
+        PA.xc = pro->xc;
+        PA.C = pro->C;
+        PA.lox = pro->M.lo[0];
+        PA.cox = pro->M.co[0];
+        PA.loy = pro->M.lo[1];
+        PA.coy = pro->M.co[1];
+        PA.w = pro->w;
+    }
     if (partial)
-        gs_fused2_kernel<true><<<grid, THREADS, SMEM_RES, st>>>(*m, KB, L, lout, f, jt0, ntx,
-                                                                ntx * nty, g_test_jitter, partial);
+        gs_fused2_kernel<1><<<grid, THREADS, SMEM_RES, st>>>(*m, KB, L, lout, f, jt0, ntx, ntx * nty,
+                                                             g_test_jitter, partial, PA);
+    else if (pro)
+        gs_fused2_kernel<2><<<grid, THREADS, SMEM_PRO, st>>>(*m, KB, L, lout, f, jt0, ntx, ntx * nty,
+                                                             g_test_jitter, nullptr, PA);
     else
-        gs_fused2_kernel<false><<<grid, THREADS, SMEM, st>>>(*m, KB, L, lout, f, jt0, ntx,
-                                                             ntx * nty, g_test_jitter, nullptr);
+        gs_fused2_kernel<0><<<grid, THREADS, SMEM, st>>>(*m, KB, L, lout, f, jt0, ntx, ntx * nty,
+                                                         g_test_jitter, nullptr, PA);
     return grid;
 }
 

@@ -274,6 +274,7 @@ namespace wd {
 std::atomic<long long> g_launches{0};
 int g_gs_v2 = 1;
 int g_test_jitter = 0, g_test_gs_grid = 0;
+int g_fuse_prolong = 1;
 int g_apply_variant = 1;
 int g_galerkin_generic = 0;
 }
@@ -649,10 +650,14 @@ int alloc_level(wd_ctx* ctx, Level& lv) {
 
 // one fused sweep lam -> lam2 of a level (k_gs_fused2.cu unless disabled or
 // the level is too large for 32-bit offsets); partial: also ||f - K lam||^2
-int gs_sweep_level(Level& F, cudaStream_t st, double* partial = nullptr) {
-    if (g_gs_v2 && F.L.NT < (1ll << 31) && (F.lam == F.raw[1] || F.lam == F.raw[4]))
+bool v2_level(const Level& F) {
+    return g_gs_v2 && F.L.NT < (1ll << 31) && (F.lam == F.raw[1] || F.lam == F.raw[4]);
+}
+int gs_sweep_level(Level& F, cudaStream_t st, double* partial = nullptr,
+                   const ProlongIn* pro = nullptr) {
+    if (v2_level(F))
         return launch_gs_fused2(F.L, F.coef, F.tmR[F.lam == F.raw[1] ? 0 : 1], F.lam2, F.f, st,
-                                partial);
+                                partial, pro);
     return launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st, partial);
 }
 
@@ -802,7 +807,8 @@ struct RoleGuard {
     }
 };
 
-int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st);
+int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st,
+           const ProlongIn* pro = nullptr);
 int smooth_end(wd_ctx* ctx, int l, cudaStream_t st);
 
 int coarse_solve(wd_ctx* ctx, cudaStream_t st) {
@@ -838,13 +844,13 @@ bool fused_level(const wd_ctx* ctx, int l) {
 //  * phased / line relaxation: 4 colour phases in place; on slabs the boundary
 //    rows are exchanged after phase 1 (even rows final) and phase 3 (odd rows
 //    final)
-int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st) {
+int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st, const ProlongIn* pro) {
     if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns], st, cudaEventRecordExternal));
     if (fused_level(ctx, l)) {
         RC(exchange(ctx, l, ARR_LAM, 2, st));
         for (Part& P : ctx->parts) {
             Level& F = P.lev[l];
-            gs_sweep_level(F, st);
+            gs_sweep_level(F, st, nullptr, pro);
             std::swap(F.lam, F.lam2);
         }
     } else {
@@ -904,6 +910,17 @@ bool lagged_residual(const wd_ctx* ctx) {
 
 // first = 1: the first level-0 pre-smoothing sweep has already run
 // (smooth_first_res or smooth), continue the cycle from there
+// can the prolongation of transition l -> l+1 be folded into level l's first
+// post-smoothing sweep (k_gs_fused2.cu PRO)?  One part, the fused TMA sweep on
+// level l, a horizontal transition with an identity z map (the coarse region
+// under a tile is then <= 40 x 8); env WD_FUSE_PROLONG=0 keeps the pass
+bool fuse_prolong(const wd_ctx* ctx, int l) {
+    if (!g_fuse_prolong || ctx->parts.size() != 1 || ctx->mode != MODE_SINGLE) return false;
+    if (!fused_level(ctx, l) || ctx->opt.post_smooth < 1) return false;
+    const Level& F = ctx->parts[0].lev[l];
+    return v2_level(F) && F.hflag && F.nkept == F.L.n3;
+}
+
 int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st, int first = 0) {
     Nvtx nv("level %d", l);
     if (l == ctx->nlev - 1) {
@@ -931,16 +948,27 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st, int first = 0) {
     CKL();
     n_res.end();
     RC(vcycle_level(ctx, l + 1, st));
-    Nvtx n_pro("prolongation");
-    for (Part& P : ctx->parts) {
-        Level& F = P.lev[l];
-        Level& C = P.lev[l + 1];
-        launch_prolong(F.L, C.L, F.M, C.lam, F.lam, F.nkept == F.L.n3, st, ctx->corr_w);
+    const bool fpro = fuse_prolong(ctx, l);
+    ProlongIn pro{};
+    if (fpro) {   // folded into the first post-smoothing sweep
+        Level& F = ctx->parts[0].lev[l];
+        Level& C = ctx->parts[0].lev[l + 1];
+        pro.xc = C.lam;
+        pro.C = C.L;
+        pro.M = F.M;
+        pro.w = ctx->corr_w;
+    } else {
+        Nvtx n_pro("prolongation");
+        for (Part& P : ctx->parts) {
+            Level& F = P.lev[l];
+            Level& C = P.lev[l + 1];
+            launch_prolong(F.L, C.L, F.M, C.lam, F.lam, F.nkept == F.L.n3, st, ctx->corr_w);
+        }
+        RC(exchange(ctx, l, ARR_LAM, 1, st));
     }
-    RC(exchange(ctx, l, ARR_LAM, 1, st));
-    n_pro.end();
-    Nvtx n_post("post-smoothing");
-    for (int s = 0; s < ctx->opt.post_smooth; s++, ns++) RC(smooth(ctx, l, prof, ns, st));
+    Nvtx n_post(fpro ? "post-smoothing (+ prolongation)" : "post-smoothing");
+    for (int s = 0; s < ctx->opt.post_smooth; s++, ns++)
+        RC(smooth(ctx, l, prof, ns, st, (fpro && s == 0) ? &pro : nullptr));
     RC(smooth_end(ctx, l, st));
     CKL();
     return WD_OK;
@@ -1677,6 +1705,7 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
     g_galerkin_generic = getenv("WD_GALERKIN_GENERIC") ? atoi(getenv("WD_GALERKIN_GENERIC")) : 0;
     g_gs_v2 = getenv("WD_GS_V2") ? atoi(getenv("WD_GS_V2")) : 1;
     g_test_jitter = getenv("WD_TEST_JITTER") ? atoi(getenv("WD_TEST_JITTER")) : 0;
+    g_fuse_prolong = getenv("WD_FUSE_PROLONG") ? atoi(getenv("WD_FUSE_PROLONG")) : 1;
     g_test_gs_grid = getenv("WD_TEST_GS_GRID") ? atoi(getenv("WD_TEST_GS_GRID")) : 0;
     if (!X || !Y || !Z) return fail(WD_E_INVAL, "NULL coordinate array");
     if (n1 < 3 || n2 < 3 || n3 < 2) return fail(WD_E_INVAL, "dims (%d,%d,%d): need n1,n2 >= 3, n3 >= 2", n1, n2, n3);

@@ -29,6 +29,7 @@ extern int g_tma_debug;
 // pipeline step in the fused sweep and the TMA residual; WD_TEST_GS_GRID: cap
 // on their persistent CTA count); 0 = off
 extern int g_test_jitter, g_test_gs_grid;
+extern int g_fuse_prolong;   // env WD_FUSE_PROLONG=0: keep the prolongation pass
 extern int g_galerkin_generic;   // env WD_GALERKIN_GENERIC=1: disable the unrolled path (tests)
 
 typedef long long i64;
@@ -158,8 +159,17 @@ int gs_fused_prepare();
 extern int g_gs_v2;   // env WD_GS_V2=0: use k_gs_fused.cu
 int make_ring_map(const LevDev& L, const double* v, void* map);
 int gs_fused2_prepare();
+// the prolongation folded into a sweep: lin + w P xc is the sweep's input
+// (identity-z transitions with horizontal coarsening only; k_gs_fused2.cu)
+struct ProlongIn {
+    const double* xc;
+    LevDev C;
+    MapDev M;
+    double w;
+};
 int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map, double* lout,
-                     const double* f, cudaStream_t st, double* partial = nullptr);
+                     const double* f, cudaStream_t st, double* partial = nullptr,
+                     const ProlongIn* pro = nullptr);
 
 // k_io.cu: steps either side of the path
 void launch_build_mesh(const double* zs, int n1, int n2, int n3, double x0, double y0, double dx,
