@@ -48,6 +48,7 @@ constexpr int SH = TJ + 3;          // ring rows J0-1 .. J0+TJ+1
 constexpr int PLD = RW * SH;        // doubles of one TMA box (one plane of the ring)
 constexpr int PL = (PLD + 15) / 16 * 16;   // ring plane pitch (128-byte aligned TMA destinations)
 constexpr int RING = 12;            // planes in the ring (>= LA + 8: colour 3 reads plane s-7)
+constexpr int RING_PRO = 13, LA_PRO = 5;   // PRO: one more plane in flight (see below)
 constexpr int LAG = 2;              // plane lag between consecutive colours
 constexpr int LA = 4;               // lambda planes loaded ahead
 constexpr unsigned BOX_BYTES = PLD * 8;
@@ -60,9 +61,13 @@ constexpr int THREADS = 32 * (W3 + 2);   // 18 colour warps, 1 halo warp, 1 TMA 
 constexpr int SHADOW = 8;
 constexpr size_t SMEM = sizeof(double) * PL * RING + 8 * RING + 128;
 constexpr size_t SMEM_RES = SMEM + sizeof(double) * PL * SHADOW;
-constexpr int CXM = 40, CYM = 8, CPL = CXM * CYM;   // PRO: coarse region under a tile
-// PRO: two coarse planes + the x / y tables of the ring's columns and rows
-constexpr size_t SMEM_PRO = SMEM + sizeof(double) * 2 * CPL + sizeof(int) * (RW + SH + 16);
+// PRO (fused prolongation): coarse region under a tile (<= CXM x CYM per
+// plane, two planes), the ring-column / ring-row parent tables and the coarse
+// origin of two tiles
+constexpr int CXM = 40, CYM = 8, CPL = CXM * CYM;
+constexpr int PTAB = RW + SH + 2;   // ints per tile: xtab, ytab, (cI0, cJ0)
+constexpr size_t SMEM_PRO = sizeof(double) * PL * RING_PRO + 8 * RING_PRO + 128 +
+                            sizeof(double) * 2 * CPL + sizeof(int) * 2 * PTAB + 64;
 static_assert(NHALO <= 32, "halo columns must fit one warp");
 static_assert(RING >= LA + 8, "ring too short");
 
@@ -105,18 +110,19 @@ __device__ __forceinline__ void tma4(void* dst, const CUtensorMap* m, int c0, in
         : "memory");
 }
 
-// Fused prolongation (PRO variant, the first post-smoothing sweep of a level
-// whose transition to the next level is horizontal with an identity z map):
-// the sweep's input is lambda + w P lambda_c (Eq. (7) "u <- u + P u_c",
-// P:176-181) formed in the ring as each plane lands, so the separate
-// prolongation pass (lambda read + write) disappears.  The producer warp
-// stages the coarse values under the tile (<= CXM x CYM per plane, one plane
-// ahead by cp.async) and corrects every free node of a landed ring plane with
-// exactly prolong_kernel's operations (bitwise equal to prolong + sweep).
+// Fused prolongation (PRO variant: the first post-smoothing sweep of a level
+// whose transition to the next level is horizontal with an identity z map).
+// The sweep's input is lambda + w P lambda_c (Eq. (7) "u <- u + P u_c",
+// P:176-181), formed in the ring: during step s every thread corrects its
+// share of the ring plane s + 2 (landed: the producer waited for it at the end
+// of step s - 1, one plane further ahead than the plain sweep, hence the
+// 13-plane ring and 5 planes in flight) from the coarse values under the tile,
+// staged the step before by cp.async, with exactly prolong_kernel's
+// operations -- bitwise equal to the prolongation pass followed by the sweep.
 struct ProArgs {
     const double* xc;         // coarse lambda (i-split layout of level C)
     LevDev C;                 // the coarse level
-    const int* lox;           // fine index -> lower parent (x), coincident flag
+    const int* lox;           // fine index -> lower parent, coincident flag (x, y)
     const int* cox;
     const int* loy;
     const int* coy;
@@ -139,13 +145,15 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
                  int ntx, int ntiles, int jitter, double* __restrict__ partial,
                  const __grid_constant__ ProArgs PA) {
     constexpr bool RES = MODE == 1, PRO = MODE == 2;
+    constexpr int RING = PRO ? RING_PRO : ::wd::RING;
+    constexpr int LA = PRO ? LA_PRO : ::wd::LA;
+    static_assert(RING >= LA + 8, "ring too short");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* ring = reinterpret_cast<double*>(smem_raw + ((128 - (sa(smem_raw) & 127)) & 127));
     double* shadow = ring + PL * RING;
-    double* csm = ring + PL * RING;                           // PRO: coarse planes [2][CPL]
-    int* xtab = reinterpret_cast<int*>(csm + 2 * CPL);          // PRO: per ring column (RW)
-    int* ytab = xtab + RW;                                      // PRO: per ring row (SH)
-    constexpr int EXTRA = RES ? PL * SHADOW : PRO ? 2 * CPL + (RW + SH + 16) / 2 : 0;
+    double* csm = ring + PL * RING;                             // PRO: [2][CPL]
+    int* ptab = reinterpret_cast<int*>(csm + 2 * CPL);          // PRO: [2][PTAB]
+    constexpr int EXTRA = RES ? PL * SHADOW : PRO ? 2 * CPL + PTAB + 8 : 0;
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + PL * RING + EXTRA);
     for (int t = threadIdx.x; t < PL * RING + (RES ? PL * SHADOW : PRO ? 2 * CPL : 0); t += THREADS)
         ring[t] = 0.0;
@@ -211,22 +219,39 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
         if (++lslot == RING) lslot = 0;
         if (++zl == n3) { zl = 0; ++kl; }
     };
-    // PRO (producer warp, all 32 lanes): coarse region origin of a tile, the
-    // column / row tables, the staging of one coarse plane and the correction
-    const bool prow = PRO && w == W3 + 1;
-    int pcI0 = 0, pcJ0 = 0, ptile = -1;   // tile whose tables are in xtab / ytab
-    auto coarse_origin = [&](int tk, int& cI0, int& cJ0) {
+    // ---- PRO helpers (every thread takes a share)
+    // tables of tile tk (in buffer tk & 1): ring column r -> (coarse x index
+    // relative to the tile's coarse origin << 1 | two parents), -1 if the
+    // column is not free; ring row rj likewise for y; then (cI0, cJ0)
+    auto build_tables = [&](int tk) {
         int I0, J0;
         origin(tk, I0, J0);
-        cI0 = __ldg(PA.lox + max(I0 - 4, 0));
-        cJ0 = __ldg(PA.loy + max(J0 - 1, 0));
+        int* t = ptab + (tk & 1) * PTAB;
+        const int cI0 = __ldg(PA.lox + max(I0 - 4, 0)), cJ0 = __ldg(PA.loy + max(J0 - 1, 0));
+        for (int r = threadIdx.x; r < PTAB; r += THREADS) {
+            int v = -1;
+            if (r < RW) {   // column: half = r / SW, pos = r % SW
+                const int i = I0 - 4 + 2 * (r % SW) + r / SW;
+                if (i >= 1 && i <= L.n1 - 2)
+                    v = ((__ldg(PA.lox + i) - cI0) << 1) | (__ldg(PA.cox + i) ? 0 : 1);
+            } else if (r < RW + SH) {
+                const int j = J0 - 1 + (r - RW);
+                if (j >= 0 && j < L.n2 && row_free(L, j))
+                    v = ((__ldg(PA.loy + j) - cJ0) << 1) | (__ldg(PA.coy + j) ? 0 : 1);
+            } else {
+                v = r == RW + SH ? cI0 : cJ0;
+            }
+            t[r] = v;
+        }
     };
-    auto stage_coarse = [&](int q) {   // plane q's coarse values -> csm[q & 1] (cp.async)
+    // coarse values of plane q (tile q / n3, plane z) -> csm[q & 1] (cp.async;
+    // the tile's tables must be built and visible)
+    auto stage_coarse = [&](int q) {
         const int tk = q / n3, z = q - tk * n3;
-        int cI0, cJ0;
-        coarse_origin(tk, cI0, cJ0);
+        const int* t = ptab + (tk & 1) * PTAB;
+        const int cI0 = t[RW + SH], cJ0 = t[RW + SH + 1];
         double* dst = csm + (q & 1) * CPL;
-        for (int e = lane; e < CPL; e += 32) {
+        for (int e = threadIdx.x; e < CPL; e += THREADS) {
             const int I = cI0 + e % CXM, J = cJ0 + e / CXM;
             if (I < PA.C.n1 && J < PA.C.n2 && z < PA.C.n3) {
                 const unsigned sd = (unsigned)__cvta_generic_to_shared(dst + e);
@@ -238,54 +263,31 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    auto build_tables = [&](int tk) {   // ring column r / row rj -> packed parent info
-        int I0, J0;
-        origin(tk, I0, J0);
-        coarse_origin(tk, pcI0, pcJ0);
-        for (int r = lane; r < RW + SH; r += 32) {
-            if (r < RW) {   // column: half = r / SW, pos = r % SW
-                const int i = I0 - 4 + 2 * (r % SW) + r / SW;
-                int v = -1;
-                if (i >= 1 && i <= L.n1 - 2)
-                    v = ((__ldg(PA.lox + i) - pcI0) << 1) | (__ldg(PA.cox + i) ? 0 : 1);
-                xtab[r] = v;
-            } else {
-                const int rj = r - RW, j = J0 - 1 + rj;
-                int v = -1;
-                if (j >= 0 && j < L.n2 && row_free(L, j))
-                    v = ((__ldg(PA.loy + j) - pcJ0) << 1) | (__ldg(PA.coy + j) ? 0 : 1);
-                ytab[rj] = v;
-            }
-        }
-        ptile = tk;
-    };
-    // ring plane q (landed) += w P (coarse plane q), on its free nodes; same
-    // operations as prolong_kernel's identity-z path (bitwise equal)
+    // ring plane q += w P (coarse plane q) on its free nodes (prolong_kernel's
+    // identity-z operations, bitwise equal)
     auto correct_plane = [&](int q) {
         const int tk = q / n3, z = q - tk * n3;
-        if (tk != ptile) build_tables(tk);
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        __syncwarp();
         if (z >= nz) return;
+        const int* t = ptab + (tk & 1) * PTAB;
         const double* cs = csm + (q & 1) * CPL;
         double* rp = ring + (q % RING) * PL;
-        for (int e = lane; e < PLD; e += 32) {
+        for (int e = threadIdx.x; e < PLD; e += THREADS) {
             const int rj = e / RW, r = e - rj * RW;
-            const int xt = xtab[r], yt = ytab[rj];
+            const int xt = t[r], yt = t[RW + rj];
             if (xt < 0 || yt < 0) continue;
-            const int ix = xt >> 1, iy = yt >> 1;
             const bool two = xt & 1, ny2 = yt & 1;
             const double wx = two ? 0.5 : 1.0, wy = ny2 ? 0.5 : 1.0;
-            const double* c0 = cs + iy * CXM + ix;
-            double sr = 0.0 + c0[0];
-            sr += two ? c0[1] : -0.0;
+            const double* c0 = cs + (yt >> 1) * CXM + (xt >> 1);
+            const double a0 = c0[0], a1 = c0[1], a2 = c0[CXM], a3 = c0[CXM + 1], x = rp[e];
+            double sr = 0.0 + a0;
+            sr += two ? a1 : -0.0;
             double sv = fma(wy * 1.0, wx * sr, 0.0);
             if (ny2) {
-                double sr2 = 0.0 + c0[CXM];
-                sr2 += two ? c0[CXM + 1] : -0.0;
+                double sr2 = 0.0 + a2;
+                sr2 += two ? a3 : -0.0;
                 sv = fma(wy * 1.0, wx * sr2, sv);
             }
-            rp[e] = fma(PA.w, sv, rp[e]);
+            rp[e] = fma(PA.w, sv, x);
         }
     };
     __syncthreads();   // ring zeroed, barriers initialised
@@ -295,15 +297,18 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
     // barrier carries them on), so the 608 threads do not poll the mbarriers.
     if (threadIdx.x == PRODUCER) {
         for (int p = 0; p < LA && p < G; p++) issue();
-        for (int p = 0; p < 2 && p < G; p++) mbar_wait(&full[p], 0);
+        for (int p = 0; p < (PRO ? 3 : 2) && p < G; p++) mbar_wait(&full[p], 0);
     }
-    if (prow) {   // planes 0 and 1 corrected before the first step, plane 2 staged
-        __syncwarp();
-        for (int p = 0; p < 2 && p < G; p++) {
+    if (PRO && G > 0) {   // planes 0 and 1 corrected, plane 2's coarse values staged
+        build_tables(0);
+        if (n3 <= 3 && ntk > 1) build_tables(1);   // tile 1 starts within planes 0..3
+        __syncthreads();
+        for (int p = 0; p < 3 && p < G; p++) {
             stage_coarse(p);
-            correct_plane(p);
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            __syncthreads();
+            if (p < 2) correct_plane(p);
         }
-        if (2 < G) stage_coarse(2);
     }
     __syncthreads();
 
@@ -407,18 +412,28 @@ gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__
                 zn = 0;
                 if (++kn < ntk) set_tile(kn);
             }
+            if (PRO) {   // this thread's share of plane s + 2, staging of plane s + 3
+                if (s + 2 < G) correct_plane(s + 2);
+                if (s + 3 < G) stage_coarse(s + 3);
+            }
             if (g + 1 < G && zn < nz && act) load_k(zn);
-        } else if (g == -1 && act && G > 0) {
-            load_k(0);
+        } else {
+            if (PRO) {
+                if (s + 2 < G) correct_plane(s + 2);
+                if (s + 3 < G) stage_coarse(s + 3);
+            }
+            if (g == -1 && act && G > 0) load_k(0);
         }
-        // the newest plane read at step s + 1 is s + 2 (colour 0's plane above)
-        if (threadIdx.x == PRODUCER && s + 2 < G)
-            mbar_wait(&full[(s + 2) % RING], ((s + 2) / RING) & 1);
-        if (prow && s + 2 < G) {   // correct plane s + 2, stage the coarse plane s + 3
-            __syncwarp();
-            correct_plane(s + 2);
-            if (s + 3 < G) stage_coarse(s + 3);
+        if (PRO) {
+            // the tables of the tile whose first plane is staged at step s + 1
+            const int q = s + 4;
+            if (q < G && q % n3 == 0) build_tables(q / n3);
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
+        // the newest plane read at step s + 1 is s + 2 (colour 0's plane above);
+        // PRO corrects plane s + 3 during step s + 1, so it waits one plane ahead
+        const int qw = s + (PRO ? 3 : 2);
+        if (threadIdx.x == PRODUCER && qw < G) mbar_wait(&full[qw % RING], (qw / RING) & 1);
         __syncthreads();
     }
     if (RES) {
