@@ -274,7 +274,7 @@ namespace wd {
 std::atomic<long long> g_launches{0};
 int g_gs_v2 = 1;
 int g_test_jitter = 0, g_test_gs_grid = 0;
-int g_fuse_prolong = 1;
+int g_fuse_prolong = 0;
 int g_apply_variant = 1;
 int g_galerkin_generic = 0;
 }
@@ -913,7 +913,10 @@ bool lagged_residual(const wd_ctx* ctx) {
 // can the prolongation of transition l -> l+1 be folded into level l's first
 // post-smoothing sweep (k_gs_fused2.cu PRO)?  One part, the fused TMA sweep on
 // level l, a horizontal transition with an identity z map (the coarse region
-// under a tile is then <= 40 x 8); env WD_FUSE_PROLONG=0 keeps the pass
+// under a tile is then <= 40 x 8).  Off by default (env WD_FUSE_PROLONG=1 turns
+// it on): bitwise equal, but measured slower -- Paper-scale V-cycle 32.3 ms
+// folded against 30.8 ms with the separate pass: the sweep's per-step critical
+// path grows by more than the 0.6-ms pass it saves
 bool fuse_prolong(const wd_ctx* ctx, int l) {
     if (!g_fuse_prolong || ctx->parts.size() != 1 || ctx->mode != MODE_SINGLE) return false;
     if (!fused_level(ctx, l) || ctx->opt.post_smooth < 1) return false;
@@ -1705,7 +1708,7 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
     g_galerkin_generic = getenv("WD_GALERKIN_GENERIC") ? atoi(getenv("WD_GALERKIN_GENERIC")) : 0;
     g_gs_v2 = getenv("WD_GS_V2") ? atoi(getenv("WD_GS_V2")) : 1;
     g_test_jitter = getenv("WD_TEST_JITTER") ? atoi(getenv("WD_TEST_JITTER")) : 0;
-    g_fuse_prolong = getenv("WD_FUSE_PROLONG") ? atoi(getenv("WD_FUSE_PROLONG")) : 1;
+    g_fuse_prolong = getenv("WD_FUSE_PROLONG") ? atoi(getenv("WD_FUSE_PROLONG")) : 0;
     g_test_gs_grid = getenv("WD_TEST_GS_GRID") ? atoi(getenv("WD_TEST_GS_GRID")) : 0;
     if (!X || !Y || !Z) return fail(WD_E_INVAL, "NULL coordinate array");
     if (n1 < 3 || n2 < 3 || n3 < 2) return fail(WD_E_INVAL, "dims (%d,%d,%d): need n1,n2 >= 3, n3 >= 2", n1, n2, n3);

@@ -29,7 +29,7 @@ extern int g_tma_debug;
 // pipeline step in the fused sweep and the TMA residual; WD_TEST_GS_GRID: cap
 // on their persistent CTA count); 0 = off
 extern int g_test_jitter, g_test_gs_grid;
-extern int g_fuse_prolong;   // env WD_FUSE_PROLONG=0: keep the prolongation pass
+extern int g_fuse_prolong;   // env WD_FUSE_PROLONG=1: fold the prolongation into the sweep
 extern int g_galerkin_generic;   // env WD_GALERKIN_GENERIC=1: disable the unrolled path (tests)
 
 typedef long long i64;

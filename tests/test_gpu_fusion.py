@@ -1,10 +1,10 @@
 """The prolongation folded into the first post-smoothing sweep (k_gs_fused2.cu
-PRO variant; Eq. (7) "u <- u + P u_c") against the separate
-prolongation pass (env WD_FUSE_PROLONG=0): every V-cycle iterate and the whole
-solve bitwise equal, on grids whose transitions fold (horizontal, identity z)
-and mix with ones that do not (vertical merging), with ragged tails.  The
-oracle parity of the fused path is covered by tests/test_gpu_parity.py (the
-default options fold)."""
+PRO variant, env WD_FUSE_PROLONG=1; Eq. (7) "u <- u + P u_c")
+against the separate prolongation pass (the default): every V-cycle iterate
+and the whole solve bitwise equal, on grids whose transitions fold
+(horizontal, identity z) and mix with ones that do not (vertical merging),
+with ragged tails.  The oracle parity of the default path is covered by
+tests/test_gpu_parity.py; bitwise equality carries it over to the folded one."""
 import os
 
 import pytest
@@ -66,4 +66,4 @@ def test_fused_prolongation_bitwise(wd, grid):
         a.close()
         b.close()
     finally:
-        _ctx(wd, p, True).close()   # the knob is read at assembly: back to the default
+        _ctx(wd, p, False).close()   # the knob is read at assembly: back to the default
