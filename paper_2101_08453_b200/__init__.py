@@ -110,7 +110,7 @@ ABI_SYMBOLS = ["wd_default_options", "wd_assemble", "wd_rhs", "wd_vcycle", "wd_s
                "wd_residual_norm", "wd_profile_read", "wd_profile_reset", "wd_launch_count",
                "wd_bench_kernel", "wd_partition_rows", "wd_nccl_unique_id", "wd_nccl_comm_init",
                "wd_gather_level", "wd_build_mesh", "wd_interp_wind", "wd_mass_consistency",
-               "wd_downscale_step"]
+               "wd_downscale_step", "wd_plan_decomposition"]
 
 BENCH_KERNELS = {"gs_sweep": 0, "apply": 1, "restrict": 2, "prolong": 3, "vcycle": 4,
                  "residual_norm": 5, "galerkin": 6, "assemble": 7, "gs_sweep_phased": 8,
