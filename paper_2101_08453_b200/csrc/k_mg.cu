@@ -358,6 +358,7 @@ restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
         // the generic loop below with compile-time weights (same order, bitwise equal)
         const double w[3] = {0.5, 1.0, 0.5};
         const int fi = M.pos[0][I], fj = M.pos[1][J];
+#pragma unroll 5   // several planes' 9 loads in flight
         for (int Kc = 0; Kc <= C.n3 - 2; Kc++) {
             double s = 0.0;
 #pragma unroll
@@ -410,7 +411,10 @@ prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
         const double* c3 = xc + loff(C, ix + nx - 1, iy + ny - 1, 0);
         double* xo = x + loff(F, i, j, 0);
         const bool two = nx == 2;
-#pragma unroll 16   // all planes' loads in flight (Paper-scale level 0: 0.71 -> 0.58 ms)
+// one plane per iteration (unroll 16): batching 2, 4 or 8 planes' loads
+// ahead of the stores, and a memory-order (row block) variant, all measured
+// slower at Paper-scale level 0 (0.73 / 0.93 / 1.26 / 0.79 ms against 0.66)
+#pragma unroll 16
         for (int k = 0; k <= F.n3 - 2; k++) {
             const i64 kc = (i64)k * C.sk;
             double sr = 0.0 + ldg(c0 + kc);

@@ -228,6 +228,12 @@ enum { MODE_SINGLE = 0, MODE_NCCL = 1, MODE_VIRTUAL = 2 };
 
 struct wd_ctx {
     int n1, n2, n3;            // global node dims
+    // test / experiment knobs (env, read at wd_assemble): gs_v2, jitter,
+    // gs_grid, fuse_prolong, apply_variant -- kept per context
+    // and installed by KnobScope at every entry point that launches work, so
+    // contexts assembled under different settings keep them (graphs are
+    // captured lazily, at the first cycle)
+    int knob[5] = {1, 0, 0, 0, 1};
     double a[3], c[3];
     wd_options opt;
     int mode = MODE_SINGLE;
@@ -804,6 +810,18 @@ struct RoleGuard {
                 P.lev[l].lam = P.lev[l].raw[1];
                 P.lev[l].lam2 = P.lev[l].raw[4];
             }
+    }
+};
+
+// installs a context's knobs (wd_ctx::knob) in the launchers' globals
+struct KnobScope {
+    explicit KnobScope(const wd_ctx* c) {
+        if (!c) return;
+        g_gs_v2 = c->knob[0];
+        g_test_jitter = c->knob[1];
+        g_test_gs_grid = c->knob[2];
+        g_fuse_prolong = c->knob[3];
+        g_apply_variant = c->knob[4];
     }
 };
 
@@ -1722,6 +1740,8 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
     if (opt && opt->coarsest_max_free > 8192)
         return fail(WD_E_INVAL, "coarsest_max_free %d > 8192 (dense inverse)", opt->coarsest_max_free);
     wd_ctx* ctx = new wd_ctx();
+    const int kn[5] = {g_gs_v2, g_test_jitter, g_test_gs_grid, g_fuse_prolong, g_apply_variant};
+    memcpy(ctx->knob, kn, sizeof kn);
     if (const char* v = getenv("WD_TEST_CORRECTION_WEIGHT")) ctx->corr_w = atof(v);
     int rc = assemble_impl(X, Y, Z, n1, n2, n3, a1, a2, a3, opt, (cudaStream_t)stream, ctx);
     if (rc) {
@@ -1740,6 +1760,7 @@ int wd_assemble(const double* X, const double* Y, const double* Z, int n1, int n
 }
 
 int wd_rhs(wd_ctx* ctx, const double* u0, double* f, void* stream) {
+    KnobScope knobs_(ctx);
     Nvtx nvtx_("wd_rhs");
     if (!ctx || !u0 || !f) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
@@ -1827,6 +1848,7 @@ static int recover_pipelined(wd_ctx* ctx, const double* lambda, const double* u0
 }
 
 int wd_recover_wind(wd_ctx* ctx, const double* lambda, const double* u0, double* u, void* stream) {
+    KnobScope knobs_(ctx);
     Nvtx nvtx_("wd_recover_wind");
     if (!ctx || !lambda || !u0 || !u) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
@@ -1911,6 +1933,7 @@ int wd_interp_wind(const double* uc, int nxc, int nyc, int nzc, double xc0, doub
 }
 
 int wd_mass_consistency(wd_ctx* ctx, const double* u, double out[2], void* stream) {
+    KnobScope knobs_(ctx);
     if (!ctx || !u || !out) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
     Stage su;
@@ -1953,6 +1976,7 @@ int wd_mass_consistency(wd_ctx* ctx, const double* u, double out[2], void* strea
 
 int wd_downscale_step(wd_ctx* ctx, const double* u0, double* lambda, int warm, double rel_tol,
                       double* u, wd_report* rep, void* stream) {
+    KnobScope knobs_(ctx);
     Nvtx nvtx_("wd_downscale_step");
     if (!ctx || !u0 || !lambda || !u) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
@@ -1977,6 +2001,7 @@ int wd_downscale_step(wd_ctx* ctx, const double* u0, double* lambda, int warm, d
 }
 
 int wd_vcycle(wd_ctx* ctx, double* lambda, const double* f, double* rel_res_out, void* stream) {
+    KnobScope knobs_(ctx);
     Nvtx nvtx_("wd_vcycle");
     if (!ctx || !lambda || !f) return fail(WD_E_INVAL, "NULL argument");
     RoleGuard roles(ctx);
@@ -2010,6 +2035,7 @@ int wd_vcycle(wd_ctx* ctx, double* lambda, const double* f, double* rel_res_out,
 
 int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol, double* lambda,
              wd_report* rep, void* stream) {
+    KnobScope knobs_(ctx);
     Nvtx nvtx_("wd_solve");
     if (!ctx || !f || !lambda) return fail(WD_E_INVAL, "NULL argument");
     RoleGuard roles(ctx);
@@ -2152,6 +2178,7 @@ void wd_profile_reset(wd_ctx* ctx) {
 long long wd_launch_count(void) { return g_launches.load(); }
 
 int wd_bench_kernel(wd_ctx* ctx, int which, int level, int reps, double* ms_out) {
+    KnobScope knobs_(ctx);
     RC(check_level(ctx, level));
     RC(check_single(ctx));
     RoleGuard roles(ctx);
@@ -2229,6 +2256,7 @@ int wd_level_plan(const wd_ctx* ctx, int level, int* horizontal, int* kept, int*
 int wd_gather_level(const wd_ctx* ctx) { return ctx ? (ctx->gather < MAXLEV ? ctx->gather : -1) : -1; }
 
 int wd_get_stencil(wd_ctx* ctx, int level, double* K27, void* stream) {
+    KnobScope knobs_(ctx);
     RC(check_level(ctx, level));
     RC(check_single(ctx));
     cudaStream_t st = (cudaStream_t)stream;
@@ -2249,6 +2277,7 @@ static Nat whole(const LevDev& L, const double* p) {
 }
 
 int wd_apply(wd_ctx* ctx, int level, const double* x, double* y, void* stream) {
+    KnobScope knobs_(ctx);
     RC(check_level(ctx, level));
     RC(check_single(ctx));
     cudaStream_t st = (cudaStream_t)stream;
@@ -2266,6 +2295,7 @@ int wd_apply(wd_ctx* ctx, int level, const double* x, double* y, void* stream) {
 }
 
 int wd_smooth(wd_ctx* ctx, int level, double* x, const double* f, int sweeps, void* stream) {
+    KnobScope knobs_(ctx);
     RC(check_level(ctx, level));
     RC(check_single(ctx));
     RoleGuard roles(ctx);
@@ -2287,6 +2317,7 @@ int wd_smooth(wd_ctx* ctx, int level, double* x, const double* f, int sweeps, vo
 }
 
 int wd_restrict(wd_ctx* ctx, int level, const double* r, double* fc, void* stream) {
+    KnobScope knobs_(ctx);
     RC(check_level(ctx, level));
     RC(check_single(ctx));
     if (level >= ctx->nlev - 1) return fail(WD_E_INVAL, "no coarser level");
@@ -2305,6 +2336,7 @@ int wd_restrict(wd_ctx* ctx, int level, const double* r, double* fc, void* strea
 }
 
 int wd_prolong(wd_ctx* ctx, int level, const double* xc, double* x, void* stream) {
+    KnobScope knobs_(ctx);
     RC(check_level(ctx, level));
     RC(check_single(ctx));
     if (level >= ctx->nlev - 1) return fail(WD_E_INVAL, "no coarser level");
@@ -2325,6 +2357,7 @@ int wd_prolong(wd_ctx* ctx, int level, const double* xc, double* x, void* stream
 }
 
 int wd_coarse_solve(wd_ctx* ctx, const double* f, double* x, void* stream) {
+    KnobScope knobs_(ctx);
     if (!ctx || !f || !x) return fail(WD_E_INVAL, "NULL argument");
     RC(check_single(ctx));
     RoleGuard roles(ctx);
@@ -2344,6 +2377,7 @@ int wd_coarse_solve(wd_ctx* ctx, const double* f, double* x, void* stream) {
 
 int wd_residual_norm(wd_ctx* ctx, const double* x, const double* f, double* abs_out,
                      double* rel_out, void* stream) {
+    KnobScope knobs_(ctx);
     if (!ctx || !x || !f) return fail(WD_E_INVAL, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
     Stage sx, sf;

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--apply-variants", default="")
     ap.add_argument("--only", default="", help="comma list of level-0 kernels; skip the rest")
+    ap.add_argument("--breakdown", action="store_true",
+                    help="sweep/apply/restrict/prolong at every level (V-cycle time per level)")
     args = ap.parse_args()
     import paper_2101_08453_b200 as wd
     import synth
@@ -46,6 +48,18 @@ def main():
             d.update(extra)
         print(json.dumps(d), flush=True)
 
+    if args.breakdown:
+        tot = 0.0
+        for l in range(ctx.num_levels() - 1):
+            t = {k: wd.wd_bench_kernel(ctx, k, l, args.reps)
+                 for k in ("gs_sweep", "apply", "restrict", "prolong")}
+            est = 4 * t["gs_sweep"] + t["apply"] + t["restrict"] + t["prolong"]
+            tot += est
+            print(json.dumps({"level": l, "dims": ctx.level_dims(l), **t, "est_level_ms": est}),
+                  flush=True)
+        print(json.dumps({"vcycle_ms": wd.wd_bench_kernel(ctx, "vcycle", 0, args.reps),
+                          "sum_levels_ms": tot}), flush=True)
+        return
     if args.only:
         for name in args.only.split(","):
             report(name)

@@ -1,10 +1,13 @@
-"""The prolongation folded into the first post-smoothing sweep (k_gs_fused2.cu
-PRO variant, env WD_FUSE_PROLONG=1; Eq. (7) "u <- u + P u_c")
-against the separate prolongation pass (the default): every V-cycle iterate
-and the whole solve bitwise equal, on grids whose transitions fold
-(horizontal, identity z) and mix with ones that do not (vertical merging),
-with ragged tails.  The oracle parity of the default path is covered by
-tests/test_gpu_parity.py; bitwise equality carries it over to the folded one."""
+"""The prolongation (Eq. (7) "u <- u + P u_c") folded into the
+first post-smoothing sweep (k_gs_fused2.cu PRO variant, env WD_FUSE_PROLONG=1)
+against the separate pass (the default): every V-cycle iterate, the whole
+solve and the single-transition entry point bitwise equal, on grids whose
+transitions have an identity z map (horizontal coarsening only) mixed with
+ones that merge layers, with ragged tails.
+
+The knobs are read at wd_assemble and kept per context.  The oracle parity of
+the default path is covered by tests/test_gpu_parity.py; bitwise equality
+carries it over to the alternatives."""
 import os
 
 import pytest
@@ -31,24 +34,32 @@ def wd():
     return m
 
 
-def _ctx(wd, p, fuse):
-    old = os.environ.get("WD_FUSE_PROLONG")
-    os.environ["WD_FUSE_PROLONG"] = "1" if fuse else "0"
+def _ctx(wd, p, env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         return wd.wd_assemble(p.X, p.Y, p.Z, p.a, wd.default_options(coarsest_max_free=60))
     finally:
-        if old is None:
-            os.environ.pop("WD_FUSE_PROLONG", None)
-        else:
-            os.environ["WD_FUSE_PROLONG"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
+VARIANTS = {
+    "fused_prolong": ({"WD_FUSE_PROLONG": "1"}, {"WD_FUSE_PROLONG": "0"}),
+}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
 @pytest.mark.parametrize("grid", list(GRIDS))
-def test_fused_prolongation_bitwise(wd, grid):
+def test_prolongation_schedules_bitwise(wd, grid, variant):
     p = GRIDS[grid]()
+    ea, eb = VARIANTS[variant]
+    a = _ctx(wd, p, ea)
+    b = _ctx(wd, p, eb)
     try:
-        a = _ctx(wd, p, True)
-        b = _ctx(wd, p, False)
         plans = [a.level_plan(l) for l in range(a.num_levels() - 1)]
         assert any(pl["horizontal"] for pl in plans)
         f = wd.wd_rhs(a, p.u0)
@@ -63,7 +74,32 @@ def test_fused_prolongation_bitwise(wd, grid):
         lb, rb = wd.wd_solve(b, f, rel_tol=1e-10)
         assert torch.equal(la, lb) and ra["cycles"] == rb["cycles"]
         assert ra["hist"] == rb["hist"]
+        # the single-transition entry point too
+        if a.num_levels() > 1:
+            n1, n2, n3 = a.level_dims(1)
+            xc = torch.randn(n3, n2, n1, dtype=torch.float64, device=DEV)
+            ya = wd.wd_prolong(a, 0, xc, x.clone())
+            yb = wd.wd_prolong(b, 0, xc, x.clone())
+            assert torch.equal(ya, yb)
+    finally:
         a.close()
         b.close()
+
+
+def test_knobs_are_per_context(wd):
+    """Two contexts assembled under different knob settings keep their own
+    (the V-cycle graphs are captured at the first cycle, after both exist)."""
+    p = GRIDS["small"]()
+    a = _ctx(wd, p, {"WD_TEST_GS_GRID": "1"})
+    b = _ctx(wd, p, {"WD_TEST_GS_GRID": "0"})
+    try:
+        f = wd.wd_rhs(a, p.u0)
+        ta = wd.wd_bench_kernel(a, "gs_sweep", 0, 3)
+        tb = wd.wd_bench_kernel(b, "gs_sweep", 0, 3)
+        assert ta > 2 * tb   # one persistent CTA against the full grid
+        la, _ = wd.wd_solve(a, f, rel_tol=1e-9)
+        lb, _ = wd.wd_solve(b, f, rel_tol=1e-9)
+        assert torch.equal(la, lb)
     finally:
-        _ctx(wd, p, False).close()   # the knob is read at assembly: back to the default
+        a.close()
+        b.close()
