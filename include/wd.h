@@ -105,6 +105,13 @@ typedef struct {
                                 vertical line relaxation (the WD_SMOOTH_LINE sweep) on the
                                 levels >= this one, `smoother` below it; -1 = `smoother` on
                                 every level (default -1) */
+    int device_loop;         /* 1: wd_solve runs its cycle loop on the device -- one CUDA graph
+                                whose conditional WHILE node repeats the cycle while a kernel's
+                                convergence test says so, no host round trip per cycle -- when
+                                the context is eligible (one GPU, fused smoother, graphs on,
+                                profile off); same iterates, history and cycle count as the
+                                host-driven loop.  Default 0 (host loop): measured no faster
+                                (scripts/device_loop_timing.py, profiles/r2_device_loop.jsonl) */
 } wd_options;
 
 typedef struct {

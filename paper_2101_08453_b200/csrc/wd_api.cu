@@ -226,6 +226,17 @@ enum { MODE_SINGLE = 0, MODE_NCCL = 1, MODE_VIRTUAL = 2 };
 
 }  // namespace
 
+// wd_solve's cycle-loop state when the loop runs on the device (see
+// build_device_loop): the host loop's locals, the report's history and the
+// number of times each conditional body ran
+struct LoopDev {
+    double fn, tol, rel0, rel1, rel_last;
+    double ring4[4];
+    double hist[256];
+    int max_cycles, c, have, first_done, status;
+    int n_first_res, n_first, n_res;
+};
+
 struct wd_ctx {
     int n1, n2, n3;            // global node dims
     // test / experiment knobs (env, read at wd_assemble): gs_v2, jitter,
@@ -261,6 +272,13 @@ struct wd_ctx {
     // (k_gs_fused.cu RES), so the convergence test needs no residual pass
     cudaGraphExec_t g_first_res = nullptr, g_first = nullptr, g_rest = nullptr;
     long long k_first_res = 0, k_first = 0, k_rest = 0;
+    // the whole cycle loop as one graph (conditional WHILE node), its kernel
+    // counts per body and the device / pinned host copies of its state
+    cudaGraphExec_t g_loop = nullptr;
+    long long kl_first_res = 0, kl_first = 0, kl_rest = 0, kl_res = 0;
+    LoopDev* loopd = nullptr;
+    LoopDev* looph = nullptr;
+    bool loop_broken = false;   // building the loop graph failed once: host loop
     long long bytes = 0;
     std::vector<std::pair<void*, size_t>> pool;   // staging buffers for host pointers
     std::vector<int> pool_busy;
@@ -1160,6 +1178,200 @@ int norm_sq(wd_ctx* ctx, int which, int slot, cudaStream_t st) {
     return WD_OK;
 }
 
+// ------------------------------------------------------------ device loop
+// wd_solve's cycle loop as one CUDA graph.  The host loop below it runs, per
+// cycle: test -> [first sweep] -> rest of the cycle -> [residual pass | first
+// sweep of the next cycle returning the residual of this cycle's iterate];
+// the bracketed steps are taken or skipped on the outcome of the test and of
+// the rate prediction.  Here the same steps are bodies of conditional nodes
+// whose conditions two one-thread kernels set from the device scalars, with
+// the host loop's decisions in its order and arithmetic, so iterates,
+// history and cycle count are the host loop's bit for bit
+// (tests/test_gpu_device_loop.py):
+//
+//   top:  WHILE(hw) { test -> IF(hr) R }
+//   R:    IF(h1) first -> rest of the cycle -> post -> IF(hp) residual
+//                                                     ELSE first_res
+//
+// (a warm start's first residual-returning sweep is launched by the host
+// before the graph).  Conditional bodies may hold kernels, memsets and
+// copies only (no events), so the loop is used when profiling is off.
+struct LoopHandles {
+    cudaGraphConditionalHandle hw, hr, h1, hp;
+};
+
+// the test of iterate c: rel = ||f - K lam_c|| / ||f|| (dscal[0] = ||r||^2)
+__global__ void loop_test_kernel(LoopDev* L, const double* __restrict__ dscal, LoopHandles h) {
+    const int c = L->c;
+    const double rel = sqrt(dscal[0]) / L->fn;
+    if (c < 256) L->hist[c] = rel;
+    if (c == 0) L->rel0 = rel;
+    if (c == 1) L->rel1 = rel;
+    L->ring4[c & 3] = rel;
+    L->rel_last = rel;
+    int st;
+    if (!isfinite(rel)) st = WD_E_NONFINITE;
+    else if (rel <= L->tol) st = WD_OK;
+    else if (c >= 3 && rel > 10.0 * L->ring4[(c - 3) & 3]) st = WD_E_DIVERGED;
+    else if (c >= L->max_cycles) st = WD_E_NOCONV;
+    else st = -1;
+    L->status = st;
+    const bool go = st == -1;
+    const bool first = go && !L->first_done;   // the cycle's first sweep still to run
+    if (first) L->n_first++;
+    cudaGraphSetConditional(h.hw, go ? 1u : 0u);
+    cudaGraphSetConditional(h.hr, go ? 1u : 0u);
+    cudaGraphSetConditional(h.h1, first ? 1u : 0u);
+}
+
+// after the cycle: a separate residual pass when the last two factors
+// predict convergence, or at the cycle cap; else the next cycle's first
+// sweep, which returns the residual of this cycle's iterate
+__global__ void loop_post_kernel(LoopDev* L, LoopHandles h) {
+    const int c = ++L->c;
+    const double rel = L->rel_last;
+    const double prev = c >= 2 ? L->ring4[(c - 2) & 3] : 0.0;
+    const bool predicted = prev > 0.0 && rel * (rel / prev) <= L->tol;
+    const bool res = predicted || c >= L->max_cycles;
+    L->first_done = res ? 0 : 1;
+    if (res) L->n_res++;
+    else L->n_first_res++;
+    cudaGraphSetConditional(h.hp, res ? 1u : 0u);   // else: the first sweep
+}
+
+// append a conditional node (handle h, one body) to the graph `st` is
+// capturing, after its current dependencies; capture continues after it
+int capture_conditional(cudaStream_t st, cudaGraphConditionalHandle h,
+                        cudaGraphConditionalNodeType type, cudaGraph_t* body,
+                        cudaGraph_t* else_body = nullptr) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+    if (cs != cudaStreamCaptureStatusActive) return fail(WD_E_CUDA, "device loop: stream not capturing");
+    cudaGraphNodeParams p = {cudaGraphNodeTypeConditional};
+    p.conditional.handle = h;
+    p.conditional.type = type;
+    p.conditional.size = else_body ? 2 : 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, deps, nd, &p));
+    *body = p.conditional.phGraph_out[0];
+    if (else_body) *else_body = p.conditional.phGraph_out[1];
+    CK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+    return WD_OK;
+}
+
+// capture fn(stream) into the existing graph g; *nk = kernels it launched
+template <class Fn>
+int capture_into(wd_ctx* ctx, cudaGraph_t g, long long* nk, Fn fn) {
+    const long long before = g_launches.load();
+    CK(cudaStreamBeginCaptureToGraph(ctx->cap, g, nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    const int rc = fn(ctx->cap);
+    cudaGraph_t out = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(ctx->cap, &out);
+    const long long d = g_launches.load() - before;
+    if (nk) *nk = d;
+    g_launches -= d;   // captured, not executed
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(WD_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    return WD_OK;
+}
+
+// build ctx->g_loop (one part, lagged residual, graphs on); buffer roles
+// canonical on entry and on return
+int build_device_loop(wd_ctx* ctx) {
+    if (!ctx->loopd) RC(dalloc(ctx, (void**)&ctx->loopd, sizeof(LoopDev)));
+    if (!ctx->looph) CK(cudaMallocHost((void**)&ctx->looph, sizeof(LoopDev)));
+    LoopDev* L = ctx->loopd;
+    const double* dscal = ctx->dscal;
+    cudaGraph_t top = nullptr;
+    CK(cudaGraphCreate(&top, 0));
+    struct Drop {
+        cudaGraph_t g;
+        ~Drop() { if (g) cudaGraphDestroy(g); }
+    } drop{top};
+    LoopHandles h;
+    CK(cudaGraphConditionalHandleCreate(&h.hw, top, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams p = {cudaGraphNodeTypeConditional};
+    p.conditional.handle = h.hw;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    CK(cudaGraphAddNode(&wnode, top, nullptr, 0, &p));
+    cudaGraph_t W = p.conditional.phGraph_out[0];
+    CK(cudaGraphConditionalHandleCreate(&h.hr, W, 0, 0));
+    cudaGraph_t R = nullptr, S1 = nullptr, SR = nullptr, S0 = nullptr;
+    // R's handles live in R, which exists once its node does: create the
+    // node first (empty body), then the handles, then capture the bodies
+    RC(capture_into(ctx, W, nullptr, [&](cudaStream_t s) -> int {
+        return capture_conditional(s, h.hr, cudaGraphCondTypeIf, &R);
+    }));
+    CK(cudaGraphConditionalHandleCreate(&h.h1, R, 0, 0));
+    CK(cudaGraphConditionalHandleCreate(&h.hp, R, 0, 0));
+    // W = test -> IF(hr) R: the test kernel goes in front of the IF node
+    {
+        cudaKernelNodeParams kp;
+        memset(&kp, 0, sizeof kp);
+        void* args[] = {(void*)&L, (void*)&dscal, (void*)&h};
+        kp.func = (void*)loop_test_kernel;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = args;
+        cudaGraphNode_t tn, rn;
+        size_t nn = 1;
+        CK(cudaGraphGetNodes(W, &rn, &nn));
+        CK(cudaGraphAddKernelNode(&tn, W, nullptr, 0, &kp));
+        CK(cudaGraphAddDependencies(W, &tn, &rn, 1));
+    }
+    // R: captured with the roles a first sweep leaves (swapped); the rest of
+    // the cycle ends canonical
+    for (Part& P : ctx->parts) std::swap(P.lev[0].lam, P.lev[0].lam2);
+    RC(capture_into(ctx, R, &ctx->kl_rest, [&](cudaStream_t s) -> int {
+        RC(capture_conditional(s, h.h1, cudaGraphCondTypeIf, &S1));
+        RC(vcycle_level(ctx, 0, s, 1));
+        loop_post_kernel<<<1, 1, 0, s>>>(L, h);
+        return capture_conditional(s, h.hp, cudaGraphCondTypeIf, &SR, &S0);
+    }));
+    for (Part& P : ctx->parts) {
+        Level& F = P.lev[0];
+        if (F.lam != F.raw[1]) std::swap(F.lam, F.lam2);
+    }
+    // S1 runs from the canonical roles, before the rest of the cycle
+    RC(capture_into(ctx, S1, &ctx->kl_first,
+                    [&](cudaStream_t s) { return smooth(ctx, 0, false, 0, s); }));
+    for (Part& P : ctx->parts) std::swap(P.lev[0].lam, P.lev[0].lam2);
+    // SR and S0 run after the rest of the cycle, from the canonical roles
+    RC(capture_into(ctx, SR, &ctx->kl_res, [&](cudaStream_t s) { return residual_sq(ctx, 0, s); }));
+    RC(capture_into(ctx, S0, &ctx->kl_first_res,
+                    [&](cudaStream_t s) { return smooth_first_res(ctx, false, s); }));
+    for (Part& P : ctx->parts) std::swap(P.lev[0].lam, P.lev[0].lam2);
+    const cudaError_t e = cudaGraphInstantiate(&ctx->g_loop, top, 0);
+    if (e != cudaSuccess) {
+        ctx->g_loop = nullptr;
+        return fail(WD_E_CUDA, "device loop instantiate: %s", cudaGetErrorString(e));
+    }
+    return WD_OK;
+}
+
+// may wd_solve run its loop on the device?  Builds the graph on first use; a
+// failed build leaves the host loop in charge for this context
+bool use_device_loop(wd_ctx* ctx, bool lag) {
+    if (!lag || !ctx->opt.device_loop || ctx->opt.profile || !ctx->opt.use_graph) return false;
+    if (ctx->parts.size() != 1 || ctx->mode != MODE_SINGLE || ctx->loop_broken) return false;
+    if (!ctx->g_loop && build_device_loop(ctx) != WD_OK) {
+        ctx->loop_broken = true;
+        cudaGetLastError();
+        for (Part& P : ctx->parts) {   // roles back to canonical
+            P.lev[0].lam = P.lev[0].raw[1];
+            P.lev[0].lam2 = P.lev[0].raw[4];
+        }
+        return false;
+    }
+    return true;
+}
+
 int fetch_scalars(wd_ctx* ctx, int n, cudaStream_t st) {
     CK(cudaMemcpyAsync(ctx->hscal, ctx->dscal, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -1235,6 +1447,7 @@ void wd_default_options(wd_options* o) {
     o->nranks = 1;
     o->smoother = WD_SMOOTH_FUSED;
     o->line_from_level = -1;
+    o->device_loop = 0;
 }
 
 const char* wd_last_error(void) { return g_err; }
@@ -1244,8 +1457,10 @@ void wd_destroy(wd_ctx* ctx) {
     cudaDeviceSynchronize();   // no work of the context may still be in flight
     cudaGetLastError();
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
-    for (cudaGraphExec_t g : {ctx->g_first_res, ctx->g_first, ctx->g_rest})
+    for (cudaGraphExec_t g : {ctx->g_first_res, ctx->g_first, ctx->g_rest, ctx->g_loop})
         if (g) cudaGraphExecDestroy(g);
+    dfree(ctx->loopd);
+    if (ctx->looph) cudaFreeHost(ctx->looph);
     if (ctx->cap) cudaStreamDestroy(ctx->cap);
     if (ctx->pin_s) cudaStreamDestroy(ctx->pin_s);
     if (ctx->pout_s) cudaStreamDestroy(ctx->pout_s);
@@ -2096,6 +2311,39 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
         for (Part& P : ctx->parts) CK(cudaMemsetAsync(P.lev[0].lam, 0, sizeof(double) * P.lev[0].L.NT, st));
         R.rel_res_hist[0] = 0.0;
         status = WD_OK;
+    } else if (use_device_loop(ctx, lag)) {
+        LoopDev* H = ctx->looph;
+        memset(H, 0, sizeof *H);
+        H->fn = fn;
+        H->tol = rel_tol;
+        H->max_cycles = ctx->opt.max_cycles;
+        H->first_done = have ? 0 : 1;
+        H->status = -1;
+        CK(cudaMemcpyAsync(ctx->loopd, H, sizeof *H, cudaMemcpyHostToDevice, st));
+        if (have)   // zero start: the residual of lam = 0 is f
+            CK(cudaMemcpyAsync(ctx->dscal, ctx->dscal + 1, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        else        // warm start: cycle 1's first sweep returns the residual of lam0
+            RC(run_split(ctx, 0, st));
+        CK(cudaGraphLaunch(ctx->g_loop, st));
+        CK(cudaMemcpyAsync(H, ctx->loopd, sizeof *H, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        c = H->c;
+        status = H->status;
+        memcpy(R.rel_res_hist, H->hist, sizeof(double) * std::min(c + 1, 256));
+        R.rel_res0 = H->rel0;
+        rel1 = H->rel1;
+        rel_last = H->rel_last;
+        // the iterate is in the canonical buffer whichever way the loop ended
+        for (Part& P : ctx->parts) {
+            P.lev[0].lam = P.lev[0].raw[1];
+            P.lev[0].lam2 = P.lev[0].raw[4];
+        }
+        // kernels executed: one test per test (c + 1), per cycle the post
+        // kernel and the rest of the cycle, plus the bodies the conditions
+        // selected (a warm start's first sweep counted by run_split)
+        g_launches += (long long)(c + 1) + (long long)c * (1 + ctx->kl_rest) +
+                      H->n_first_res * ctx->kl_first_res + H->n_first * ctx->kl_first +
+                      H->n_res * ctx->kl_res;
     } else {
         for (;;) {
             Nvtx n_cyc("cycle %d", c + 1);
