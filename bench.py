@@ -328,6 +328,7 @@ def run_ours(args, ws, rank, local):
     parts = np.zeros(4)
     cycles, gs_ms, gs_sweeps, vc_ms, vc_n, rates = 0, 0.0, 0, 0.0, 0, []
     gsr_ms, gsr_sweeps = 0.0, 0
+    ap_ms, ap_n, rs_ms, rs_n = 0.0, 0, 0.0, 0
     with Clocks(local) as clk:
         start.record(stream)
         for _ in range(args.steps):
@@ -340,6 +341,10 @@ def run_ours(args, ws, rank, local):
             gs_sweeps += int(prof["gs0_sweeps"])
             gsr_ms += prof["gs0res_ms"]
             gsr_sweeps += int(prof["gs0res_sweeps"])
+            ap_ms += prof["apply0_ms"]
+            ap_n += int(prof["apply0_launches"])
+            rs_ms += prof["resid_ms"]
+            rs_n += int(prof["resids"])
             vc_ms += prof["vcycle_ms"]
             vc_n += int(prof["vcycles"])
             info = hier_info(ctx)
@@ -386,6 +391,18 @@ def run_ours(args, ws, rank, local):
     else:
         traffic_all = traffic
 
+    # north_star's "operator/smoother kernels": every level-0 sweep and every
+    # level-0 operator pass of the timed steps (the residual before the
+    # restriction, 136 B/node; the residual-norm passes, 128 B/node: no r
+    # written), algorithmic bytes over their summed device time
+    op_bytes = gs_b * free0 * n_all * gs_per_sweep + 136 * free0 * ap_n + 128 * free0 * rs_n
+    op_ms = gs_ms + gsr_ms + ap_ms + rs_ms
+    op_gbs = op_bytes / (op_ms * 1e-3) / 1e9 if op_ms > 0 else 0.0
+    op_obj = {"kernels": f"{gs_name} (plain + residual variant) + apply_tma_kernel (residual "
+                         "before the restriction; residual-norm passes), level 0",
+              "achieved": op_gbs, "frac": op_gbs / peak, "ms": op_ms,
+              "launches": n_all * gs_per_sweep + ap_n + rs_n}
+
     line = None
     if rank == 0:
         line = {
@@ -423,7 +440,8 @@ def run_ours(args, ws, rank, local):
                                               "traffic": traffic_res,
                                               "frac": (bytes_launch / (res_ms * 1e-3) / 1e9 / peak
                                                        if res_ms else None)},
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         "level0_operator_smoother": op_obj},
             "gpu_launches": int(launches), "clocks": clk.summary(),
         }
     # end to end through the ABI with host (pinned) buffers

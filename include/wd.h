@@ -250,8 +250,10 @@ int wd_residual_norm(wd_ctx* ctx, const double* x, const double* f, double* abs_
  *   out[4] ms in residual-norm passes        out[5] residual-norm passes
  *   out[6] ms in level-0 sweeps that also return the residual of their input
  *          (the first sweep of a cycle in wd_solve)   out[7] their number
+ *   out[8] ms in the level-0 residual r = f - K lambda before the restriction
+ *          (one per V-cycle)                 out[9] their number
  * A sweep is one launch of the fused smoother (four launches with
- * WD_SMOOTH_PHASED).  Returns the number of values written (<= n, <= 8). */
+ * WD_SMOOTH_PHASED).  Returns the number of values written (<= n, <= 10). */
 int wd_profile_read(const wd_ctx* ctx, double* out, int n);
 /* Reset the accumulated profile. */
 void wd_profile_reset(wd_ctx* ctx);

@@ -287,7 +287,8 @@ struct wd_ctx {
     cudaEvent_t ev_cyc[2] = {};
     bool first_res = false;    // the last cycle's first sweep was the residual variant
     cudaEvent_t ev_res[2] = {};
-    double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaEvent_t ev_ap[2] = {};   // the level-0 residual before the restriction
+    double prof[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     // weight w of the coarse-grid correction lam += w P lam_c: 1 (Eq. (7));
     // env WD_TEST_CORRECTION_WEIGHT sets another value, only so that the tests
     // can drive a cycle to divergence and exercise the WD_E_DIVERGED guard
@@ -974,7 +975,9 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st, int first = 0) {
         RC(smooth_end(ctx, l, st));
     }
     Nvtx n_res("residual + restriction");
+    if (prof) CK(cudaEventRecordWithFlags(ctx->ev_ap[0], st, cudaEventRecordExternal));
     for (Part& P : ctx->parts) apply_level(P.lev[l], true, nullptr, st);
+    if (prof) CK(cudaEventRecordWithFlags(ctx->ev_ap[1], st, cudaEventRecordExternal));
     RC(exchange(ctx, l, ARR_R, 1, st));
     for (Part& P : ctx->parts) {
         Level& F = P.lev[l];
@@ -1034,6 +1037,11 @@ void profile_accumulate(wd_ctx* ctx, bool cycle, bool resid) {
         if (cudaEventElapsedTime(&ms, ctx->ev_cyc[0], ctx->ev_cyc[1]) == cudaSuccess) {
             ctx->prof[2] += ms;
             ctx->prof[3] += 1;
+        }
+        if (ctx->nlev > 1 && ctx->parts.size() == 1 &&
+            cudaEventElapsedTime(&ms, ctx->ev_ap[0], ctx->ev_ap[1]) == cudaSuccess) {
+            ctx->prof[8] += ms;
+            ctx->prof[9] += 1;
         }
     }
     if (resid && cudaEventElapsedTime(&ms, ctx->ev_res[0], ctx->ev_res[1]) == cudaSuccess) {
@@ -1468,6 +1476,7 @@ void wd_destroy(wd_ctx* ctx) {
     for (auto e : ctx->ev_gs) if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_cyc) if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_res) if (e) cudaEventDestroy(e);
+    for (auto e : ctx->ev_ap) if (e) cudaEventDestroy(e);
     for (Part& P : ctx->parts) {
         for (int l = 0; l < ctx->nlev; l++) {
             for (double* p : P.lev[l].raw) dfree(p);
@@ -1666,6 +1675,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
         for (auto& e : ctx->ev_gs) CK(cudaEventCreate(&e));
         for (auto& e : ctx->ev_cyc) CK(cudaEventCreate(&e));
         for (auto& e : ctx->ev_res) CK(cudaEventCreate(&e));
+        for (auto& e : ctx->ev_ap) CK(cudaEventCreate(&e));
     }
 
     PT.mark("coordinates + ctx");
@@ -2413,7 +2423,7 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
 // ------------------------------------------------------------------ profiling
 int wd_profile_read(const wd_ctx* ctx, double* out, int n) {
     if (!ctx || !out) return 0;
-    int m = n < 8 ? n : 8;
+    int m = n < 10 ? n : 10;
     for (int t = 0; t < m; t++) out[t] = ctx->prof[t];
     return m;
 }
