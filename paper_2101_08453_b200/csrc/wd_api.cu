@@ -541,8 +541,8 @@ int plan_hierarchy(int n1, int n2, int n3, const double a[3], const wd_options& 
     H.own0g.resize(nranks);
     H.own1g.resize(nranks);
     for (int r = 0; r < nranks; r++) wd_partition_rows(n2, nranks, r, &H.own0g[r], &H.own1g[r]);
-    for (int r = 0; r < nranks; r++)
-        if (H.own1g[r] - H.own0g[r] < MIN_OWNED)
+    for (int r = 0; r < nranks; r++)   // slabs need >= MIN_OWNED rows; one GPU takes any grid
+        if (multi && H.own1g[r] - H.own0g[r] < MIN_OWNED)
             return fail(WD_E_INVAL, "rank %d owns %d rows (< %d)", r, H.own1g[r] - H.own0g[r], MIN_OWNED);
     H.part.assign(parts.size(), std::vector<PartLevel>(MAXLEV));
     for (size_t p = 0; p < parts.size(); p++) {
@@ -1602,7 +1602,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
         return fail(WD_E_INVAL, "rank %d: rows [%d,%d) differ from wd_partition_rows [%d,%d)", o.rank,
                     o.j_begin, o.j_end, ctx->own0g[o.rank], ctx->own1g[o.rank]);
     for (int r = 0; r < ctx->nranks; r++)
-        if (ctx->own1g[r] - ctx->own0g[r] < MIN_OWNED)
+        if (ctx->nranks > 1 && ctx->own1g[r] - ctx->own0g[r] < MIN_OWNED)
             return fail(WD_E_INVAL, "rank %d owns %d rows (< %d)", r, ctx->own1g[r] - ctx->own0g[r], MIN_OWNED);
     const int nparts = ctx->mode == MODE_VIRTUAL ? ctx->nranks : 1;
     ctx->parts.resize(nparts);
