@@ -26,6 +26,7 @@
 //     is one 32-bit node offset (+ the thread's x shift) scaled onto a base
 //     instead of a 64-bit multiply-add chain per load;
 //   * ring addressing: plane slots advance incrementally (no modulo per step).
+// The residual variant runs 64 x 6 tiles (Geo<TJ_RES>; see TJ_SWEEP below).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -41,35 +42,49 @@ namespace {
 
 constexpr int HI = 32;              // positions per parity per tile row (TI = 64 columns)
 constexpr int TI = 2 * HI;
-constexpr int TJ = 8;               // tile rows
 constexpr int SW = HI + 4;          // ring positions per parity per row (columns I0-4 .. I0+TI+3)
 constexpr int RW = 2 * SW;          // ring doubles per row
-constexpr int SH = TJ + 3;          // ring rows J0-1 .. J0+TJ+1
-constexpr int PLD = RW * SH;        // doubles of one TMA box (one plane of the ring)
-constexpr int PL = (PLD + 15) / 16 * 16;   // ring plane pitch (128-byte aligned TMA destinations)
 constexpr int RING = 12;            // planes in the ring (>= LA + 8: colour 3 reads plane s-7)
 constexpr int RING_PRO = 13, LA_PRO = 5;   // PRO: one more plane in flight (see below)
 constexpr int LAG = 2;              // plane lag between consecutive colours
 constexpr int LA = 4;               // lambda planes loaded ahead
-constexpr unsigned BOX_BYTES = PLD * 8;
-// colour regions: rows per colour (B) and halo columns beyond the 32 aligned ones
-constexpr int B0 = TJ / 2 + 1, B1 = TJ / 2 + 1, B2 = TJ / 2, B3 = TJ / 2;
-constexpr int W0 = B0, W1 = W0 + B1, W2 = W1 + B2, W3 = W2 + B3;   // warp ranges
-constexpr int NHALO = 3 * B0 + 2 * B1 + B2;                          // 29 halo columns
-constexpr int PRODUCER = 32 * (W3 + 1);                              // first thread of the TMA warp
-constexpr int THREADS = 32 * (W3 + 2);   // 18 colour warps, 1 halo warp, 1 TMA producer warp
 constexpr int SHADOW = 8;
-constexpr size_t SMEM = sizeof(double) * PL * RING + 8 * RING + 128;
-constexpr size_t SMEM_RES = SMEM + sizeof(double) * PL * SHADOW;
 // PRO (fused prolongation): coarse region under a tile (<= CXM x CYM per
 // plane, two planes), the ring-column / ring-row parent tables and the coarse
 // origin of two tiles
 constexpr int CXM = 40, CYM = 8, CPL = CXM * CYM;
-constexpr int PTAB = RW + SH + 2;   // ints per tile: xtab, ytab, (cI0, cJ0)
-constexpr size_t SMEM_PRO = sizeof(double) * PL * RING_PRO + 8 * RING_PRO + 128 +
-                            sizeof(double) * 2 * CPL + sizeof(int) * 2 * PTAB + 64;
-static_assert(NHALO <= 32, "halo columns must fit one warp");
 static_assert(RING >= LA + 8, "ring too short");
+
+}  // namespace
+
+// geometry of a tile of TI x TJ columns (TJ even)
+template <int TJ_>
+struct Geo {
+    static constexpr int TJ = TJ_;
+    static constexpr int SH = TJ + 3;          // ring rows J0-1 .. J0+TJ+1
+    static constexpr int PLD = RW * SH;        // doubles of one TMA box (one plane of the ring)
+    static constexpr int PL = (PLD + 15) / 16 * 16;   // ring plane pitch (128-byte aligned)
+    static constexpr unsigned BOX_BYTES = PLD * 8;
+    // colour regions: rows per colour (B) and halo columns beyond the 32 aligned ones
+    static constexpr int B0 = TJ / 2 + 1, B1 = TJ / 2 + 1, B2 = TJ / 2, B3 = TJ / 2;
+    static constexpr int W0 = B0, W1 = W0 + B1, W2 = W1 + B2, W3 = W2 + B3;   // warp ranges
+    static constexpr int NHALO = 3 * B0 + 2 * B1 + B2;       // 29 halo columns at TJ = 8
+    static constexpr int PRODUCER = 32 * (W3 + 1);           // first thread of the TMA warp
+    static constexpr int THREADS = 32 * (W3 + 2);   // colour warps, 1 halo warp, 1 TMA producer warp
+    static constexpr size_t SMEM = sizeof(double) * PL * RING + 8 * RING + 128;
+    static constexpr size_t SMEM_RES = SMEM + sizeof(double) * PL * SHADOW;
+    static constexpr int PTAB = RW + SH + 2;   // ints per tile: xtab, ytab, (cI0, cJ0)
+    static constexpr size_t SMEM_PRO = sizeof(double) * PL * RING_PRO + 8 * RING_PRO + 128 +
+                                       sizeof(double) * 2 * CPL + sizeof(int) * 2 * PTAB + 64;
+    static_assert(TJ % 2 == 0 && NHALO <= 32, "tile rows even; halo columns must fit one warp");
+};
+// The plain and PRO sweeps run 64 x 8 tiles (18 colour warps); the residual
+// variant 64 x 6 tiles (14 colour warps, 16 in all): its 8-plane shadow makes
+// it register- and L1-tighter, and at Paper-scale level 0 it measured 5.34 ms
+// on 64 x 6 against 6.08 ms on 64 x 8 (the plain sweep: 4.67 against 4.54)
+constexpr int TJ_SWEEP = 8, TJ_RES = 6;
+
+namespace {
 
 __device__ __forceinline__ uint32_t sa(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -138,13 +153,18 @@ struct KBase {
 };
 
 // MODE 0: plain sweep; 1 (RES): also ||f - K lin||^2; 2 (PRO): input lin + w P xc
-template <int MODE>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int MODE, int TJ_>
+__global__ void __launch_bounds__(Geo<TJ_>::THREADS, 1)
 gs_fused2_kernel(const __grid_constant__ CUtensorMap mL, const __grid_constant__ KBase KB,
                  LevDev L, double* __restrict__ lout, const double* __restrict__ f, int jt0,
                  int ntx, int ntiles, int jitter, double* __restrict__ partial,
                  const __grid_constant__ ProArgs PA) {
     constexpr bool RES = MODE == 1, PRO = MODE == 2;
+    using Gm = Geo<TJ_>;
+    constexpr int TJ = Gm::TJ, SH = Gm::SH, PLD = Gm::PLD, PL = Gm::PL, PTAB = Gm::PTAB;
+    constexpr int B0 = Gm::B0, B1 = Gm::B1, W0 = Gm::W0, W1 = Gm::W1, W2 = Gm::W2, W3 = Gm::W3;
+    constexpr int NHALO = Gm::NHALO, PRODUCER = Gm::PRODUCER, THREADS = Gm::THREADS;
+    constexpr unsigned BOX_BYTES = Gm::BOX_BYTES;
     constexpr int RING = PRO ? RING_PRO : ::wd::RING;
     constexpr int LA = PRO ? LA_PRO : ::wd::LA;
     static_assert(RING >= LA + 8, "ring too short");
@@ -468,13 +488,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
 // ring box of one plane: 36 positions x 2 halves x 1 plane x 11 rows; the
 // position extent is the grid's (ceil(n1/2)), so the padding of a half row
 // and everything outside the grid read as zeros
-int make_ring_map(const LevDev& L, const double* v, void* map) {
+int make_ring_map(const LevDev& L, const double* v, void* map, bool res) {
     auto enc = encode_fn2();
     if (!enc) return -1;
     cuuint64_t dims[4] = {(cuuint64_t)((L.n1 + 1) / 2), 2, (cuuint64_t)L.n3, (cuuint64_t)L.n2};
     cuuint64_t str[3] = {(cuuint64_t)L.H * 8, (cuuint64_t)L.sk * 8, (cuuint64_t)L.sj * 8};
     cuuint32_t es[4] = {1, 1, 1, 1};
-    cuuint32_t box[4] = {SW, 2, 1, SH};
+    cuuint32_t box[4] = {SW, 2, 1, (cuuint32_t)(res ? Geo<TJ_RES>::SH : Geo<TJ_SWEEP>::SH)};
     static const CUtensorMapL2promotion promo[4] = {
         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
@@ -493,36 +513,39 @@ int gs_fused2_prepare() {
     if (dev < 0 || dev >= 64) dev = 0;
     int nsm = nsm_dev[dev].load(std::memory_order_acquire);
     if (nsm > 0) return nsm;
-    cudaFuncSetAttribute(gs_fused2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    cudaFuncSetAttribute(gs_fused2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RES);
-    cudaFuncSetAttribute(gs_fused2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_PRO);
+    cudaFuncSetAttribute(gs_fused2_kernel<0, TJ_SWEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Geo<TJ_SWEEP>::SMEM);
+    cudaFuncSetAttribute(gs_fused2_kernel<1, TJ_RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Geo<TJ_RES>::SMEM_RES);
+    cudaFuncSetAttribute(gs_fused2_kernel<2, TJ_SWEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Geo<TJ_SWEEP>::SMEM_PRO);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
     nsm_dev[dev].store(nsm, std::memory_order_release);
     return nsm;
 }
 
-// one sweep lin -> lout (k_gs_fused.cu launch_gs_fused); ring_map: the
-// make_ring_map tensor map of lin
-int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map, double* lout,
-                     const double* f, cudaStream_t st, double* partial, const ProlongIn* pro) {
+// one sweep lin -> lout (k_gs_fused.cu launch_gs_fused); ring_map /
+// ring_map_res: the make_ring_map tensor maps of lin (plain / residual tiles)
+int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
+                     const void* ring_map_res, double* lout, const double* f, cudaStream_t st,
+                     double* partial, const ProlongIn* pro) {
     const int nsm = gs_fused2_prepare();
     KBase KB;
     for (int s = 0; s < 14; s++) {
-        const int dx = slot_dx(s), dy = slot_dy(s), dz = slot_dz(s);
+        const int dy = slot_dy(s), dz = slot_dz(s);
         KB.kf[s] = coef + (i64)s * L.NT;
         // backward neighbour p - d_s: row j - dy, plane z - dz (x shift per thread)
         KB.kb[s] = coef + (i64)s * L.NT - (i64)dy * L.sj - (i64)dz * L.sk;
-        (void)dx;
     }
     const int jt0 = L.own0 - ((L.own0 + L.jg0) & 1);
-    const int ntx = (L.n1 + TI - 1) / TI, nty = (L.own1 - jt0 + TJ - 1) / TJ;
+    const int tj = partial ? TJ_RES : TJ_SWEEP;
+    const int ntx = (L.n1 + TI - 1) / TI, nty = (L.own1 - jt0 + tj - 1) / tj;
     g_launches += 1;
     // persistent CTAs; tests may cap their number (env WD_TEST_GS_GRID) so that
     // other tiles share a CTA's cross-tile pipeline
     int grid = std::min(ntx * nty, nsm);
     if (g_test_gs_grid > 0) grid = std::min(grid, g_test_gs_grid);
-    const CUtensorMap* m = (const CUtensorMap*)ring_map;
     ProArgs PA{};
     if (pro) {
         PA.xc = pro->xc;
@@ -533,15 +556,21 @@ int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map, 
         PA.coy = pro->M.co[1];
         PA.w = pro->w;
     }
-    if (partial)
-        gs_fused2_kernel<1><<<grid, THREADS, SMEM_RES, st>>>(*m, KB, L, lout, f, jt0, ntx, ntx * nty,
-                                                             g_test_jitter, partial, PA);
-    else if (pro)
-        gs_fused2_kernel<2><<<grid, THREADS, SMEM_PRO, st>>>(*m, KB, L, lout, f, jt0, ntx, ntx * nty,
-                                                             g_test_jitter, nullptr, PA);
-    else
-        gs_fused2_kernel<0><<<grid, THREADS, SMEM, st>>>(*m, KB, L, lout, f, jt0, ntx, ntx * nty,
-                                                         g_test_jitter, nullptr, PA);
+    if (partial) {
+        using G = Geo<TJ_RES>;
+        gs_fused2_kernel<1, TJ_RES><<<grid, G::THREADS, G::SMEM_RES, st>>>(
+            *(const CUtensorMap*)ring_map_res, KB, L, lout, f, jt0, ntx, ntx * nty, g_test_jitter,
+            partial, PA);
+    } else {
+        using G = Geo<TJ_SWEEP>;
+        const CUtensorMap& m = *(const CUtensorMap*)ring_map;
+        if (pro)
+            gs_fused2_kernel<2, TJ_SWEEP><<<grid, G::THREADS, G::SMEM_PRO, st>>>(
+                m, KB, L, lout, f, jt0, ntx, ntx * nty, g_test_jitter, nullptr, PA);
+        else
+            gs_fused2_kernel<0, TJ_SWEEP><<<grid, G::THREADS, G::SMEM, st>>>(
+                m, KB, L, lout, f, jt0, ntx, ntx * nty, g_test_jitter, nullptr, PA);
+    }
     return grid;
 }
 

@@ -157,6 +157,7 @@ struct Level {
     MapDev M;
     alignas(64) unsigned char tmA[128], tmB[128], tmX[128], tmF[128];
     alignas(64) unsigned char tmR[2][128];   // ring maps of raw[1] and raw[4] (k_gs_fused2.cu)
+    alignas(64) unsigned char tmRr[2][128];  // the same for the residual variant's tiles
 };
 
 struct Part {
@@ -666,8 +667,10 @@ int alloc_level(wd_ctx* ctx, Level& lv) {
     // D entries of the ping-pong buffer stay 0 (the fused sweep writes free nodes only)
     CK(cudaMemset(lv.lam2, 0, sizeof(double) * nt));
     if (make_coef_maps(lv.L, lv.coef, lv.tmA, lv.tmB) || make_vec_map(lv.L, lv.lam, lv.tmX, true) ||
-        make_vec_map(lv.L, lv.f, lv.tmF, false) || make_ring_map(lv.L, lv.raw[1], lv.tmR[0]) ||
-        make_ring_map(lv.L, lv.raw[4], lv.tmR[1]))
+        make_vec_map(lv.L, lv.f, lv.tmF, false) || make_ring_map(lv.L, lv.raw[1], lv.tmR[0], false) ||
+        make_ring_map(lv.L, lv.raw[4], lv.tmR[1], false) ||
+        make_ring_map(lv.L, lv.raw[1], lv.tmRr[0], true) ||
+        make_ring_map(lv.L, lv.raw[4], lv.tmRr[1], true))
         return fail(WD_E_CUDA, "cuTensorMapEncodeTiled failed for level dims (%d,%d,%d)", lv.L.n1,
                     lv.L.n2, lv.L.n3);
     return WD_OK;
@@ -681,8 +684,10 @@ bool v2_level(const Level& F) {
 int gs_sweep_level(Level& F, cudaStream_t st, double* partial = nullptr,
                    const ProlongIn* pro = nullptr) {
     if (v2_level(F))
-        return launch_gs_fused2(F.L, F.coef, F.tmR[F.lam == F.raw[1] ? 0 : 1], F.lam2, F.f, st,
-                                partial, pro);
+    {
+        const int b = F.lam == F.raw[1] ? 0 : 1;
+        return launch_gs_fused2(F.L, F.coef, F.tmR[b], F.tmRr[b], F.lam2, F.f, st, partial, pro);
+    }
     return launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st, partial);
 }
 

@@ -155,9 +155,9 @@ int launch_gs_fused(const LevDev& L, const double* coef, const double* lin, doub
 // per-device kernel attributes; returns the device's SM count
 int gs_fused_prepare();
 // k_gs_fused2.cu: the same sweep (bitwise) with a TMA-filled lambda ring and
-// 32-bit coupling offsets (needs NT < 2^31); ring_map = make_ring_map of lin
+// 32-bit coupling offsets (needs NT < 2^31)
 extern int g_gs_v2;   // env WD_GS_V2=0: use k_gs_fused.cu
-int make_ring_map(const LevDev& L, const double* v, void* map);
+int make_ring_map(const LevDev& L, const double* v, void* map, bool res);
 int gs_fused2_prepare();
 // the prolongation folded into a sweep: lin + w P xc is the sweep's input
 // (identity-z transitions with horizontal coarsening only; k_gs_fused2.cu)
@@ -167,9 +167,11 @@ struct ProlongIn {
     MapDev M;
     double w;
 };
-int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map, double* lout,
-                     const double* f, cudaStream_t st, double* partial = nullptr,
-                     const ProlongIn* pro = nullptr);
+// ring_map / ring_map_res: make_ring_map(.., res = false / true) of lin (the
+// plain / PRO sweeps tile 64 x 8, the residual variant (partial) 64 x 6)
+int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
+                     const void* ring_map_res, double* lout, const double* f, cudaStream_t st,
+                     double* partial = nullptr, const ProlongIn* pro = nullptr);
 
 // k_io.cu: steps either side of the path
 void launch_build_mesh(const double* zs, int n1, int n2, int n3, double x0, double y0, double dx,
