@@ -232,7 +232,7 @@ assemble_kernel(const double* __restrict__ X, const double* __restrict__ Y,
 // k; h goes through a double-buffered shared plane, so one barrier per layer.
 // Coordinates: the level's local rows; u0 / f: ABI arrays (Nat); f is written
 // on the owned rows only, 0 on the Dirichlet set.
-constexpr int RTX = 32, RTY = 16, RNTH = RTX * RTY;
+constexpr int RTX = 32, RTY = 8, RNTH = RTX * RTY;   // 256 threads: 3 CTAs per SM at 79 registers (RTY = 16: 1 CTA, 3.12 -> 2.46 ms at Paper-scale)
 __global__ void __launch_bounds__(RNTH)
 rhs_kernel(const double* __restrict__ X, const double* __restrict__ Y,
            const double* __restrict__ Z, LevDev L, Nat u0, Nat f) {
