@@ -547,7 +547,9 @@ __device__ __forceinline__ double galerkin_xyreg(const LevDev& F, const double* 
     return s;
 }
 
-__global__ void __launch_bounds__(128)
+// (128, 8): <= 64 registers, 8 CTAs per SM: Paper-scale Galerkin products 12.8 -> 12.2 ms
+// (a 48- or 40-register cap spilled: 13.9 / 16.2 ms)
+__global__ void __launch_bounds__(128, 8)
 galerkin_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ KF,
                 double* __restrict__ KC, int zident, int fast) {
     const int I = blockIdx.x * 128 + threadIdx.x;
