@@ -523,60 +523,86 @@ __device__ __forceinline__ int zpairs(const MapDev& M, int fn3, int Kc, int DZ, 
 
 // K_c(I, I + (DX, DY, DZ)) for a coarse node with regular x and y supports on a
 // transition that merges layers (z map not the identity): x and y unrolled
-// with compile-time offsets, z pairs from zpairs(); the generic loop's
-// products and sums in its order (bitwise equal)
+// with compile-time offsets, z pairs from zpairs() (computed once per CTA --
+// the coarse plane is blockIdx.z -- and read from shared memory), each pair's
+// z offset dispatched to a compile-time body; the generic loop's products and
+// sums in its order (bitwise equal)
+template <int DX, int DY, int DZ>
+__device__ __forceinline__ double galerkin_zpair(const LevDev& F, const double* __restrict__ K,
+                                                 int fi, int fj, int k, double wz, double s) {
+#pragma unroll
+    for (int b = 0; b < npairs<DY>(); b++) {
+        const Pair1 py = pair<DY>(b);
+        double sr = 0.0;
+#pragma unroll
+        for (int a = 0; a < npairs<DX>(); a++) {
+            const Pair1 px = pair<DX>(a);
+            sr = fma(px.w, kget(F, K, fi + px.u, fj + py.u, k, px.v - px.u, py.v - py.u, DZ), sr);
+        }
+        s = fma(wz * py.w, sr, s);
+    }
+    return s;
+}
+
+struct ZPairs {
+    int t[9], d[9];
+    double w[9];
+    int n;
+};
+
 template <int DX, int DY>
 __device__ __forceinline__ double galerkin_xyreg(const LevDev& F, const double* __restrict__ K,
-                                                 int fi, int fj, const int (&lt)[9],
-                                                 const int (&ld)[9], const double (&lw)[9], int ln) {
+                                                 int fi, int fj, const ZPairs& zp) {
     double s = 0.0;
-    for (int c = 0; c < ln; c++) {
-        const int k = lt[c], dz = ld[c];
-#pragma unroll
-        for (int b = 0; b < npairs<DY>(); b++) {
-            const Pair1 py = pair<DY>(b);
-            double sr = 0.0;
-#pragma unroll
-            for (int a = 0; a < npairs<DX>(); a++) {
-                const Pair1 px = pair<DX>(a);
-                sr = fma(px.w, kget(F, K, fi + px.u, fj + py.u, k, px.v - px.u, py.v - py.u, dz), sr);
-            }
-            s = fma(lw[c] * py.w, sr, s);
-        }
+    for (int c = 0; c < zp.n; c++) {
+        const int k = zp.t[c], dz = zp.d[c];
+        const double wz = zp.w[c];
+        if (dz < 0) s = galerkin_zpair<DX, DY, -1>(F, K, fi, fj, k, wz, s);
+        else if (dz == 0) s = galerkin_zpair<DX, DY, 0>(F, K, fi, fj, k, wz, s);
+        else s = galerkin_zpair<DX, DY, 1>(F, K, fi, fj, k, wz, s);
     }
     return s;
 }
 
 // (128, 8): <= 64 registers, 8 CTAs per SM: Paper-scale Galerkin products 12.8 -> 12.2 ms
 // (a 48- or 40-register cap spilled: 13.9 / 16.2 ms)
+// ZID: the transition's z map is the identity (an instance per case, so that
+// the merging case's shared z-pair lists do not weigh on the other)
+template <bool ZID>
 __global__ void __launch_bounds__(128, 8)
 galerkin_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ KF,
-                double* __restrict__ KC, int zident, int fast) {
+                double* __restrict__ KC, int fast) {
     const int I = blockIdx.x * 128 + threadIdx.x;
     const int J = blockIdx.y, Kc = blockIdx.z;
+    __shared__ ZPairs zp[ZID ? 1 : 2];   // z pairs of coarse plane Kc for DZ = 0, 1 (merging)
+    if (!ZID && fast) {
+        if (threadIdx.x < 2 && Kc + (int)threadIdx.x <= C.n3 - 1) {
+            ZPairs& z = zp[threadIdx.x];
+            z.n = zpairs(M, F.n3, Kc, threadIdx.x, z.t, z.d, z.w);
+        }
+        __syncthreads();
+    }
     if (I < 1 || I > C.n1 - 2 || !row_free(C, J) || Kc > C.n3 - 2) return;
     const bool xyreg = fast && regular1d(M.pos[0], C.n1, I) && regular1d(M.pos[1], C.n2, J);
-    if (xyreg && !zident) {
+    if (!ZID && xyreg) {
         const int fi = M.pos[0][I], fj = M.pos[1][J];
-        int t0[9], d0[9], t1[9], d1[9];
-        double w0[9], w1[9];
-        const int n0 = zpairs(M, F.n3, Kc, 0, t0, d0, w0);
-        const int n1 = zpairs(M, F.n3, Kc, 1, t1, d1, w1);
+        const ZPairs& z0 = zp[0];
+        const ZPairs& z1 = zp[ZID ? 0 : 1];
         double* o = KC + loff(C, I, J, Kc);
-        o[0 * C.NT] = galerkin_xyreg<0, 0>(F, KF, fi, fj, t0, d0, w0, n0);
-        o[1 * C.NT] = galerkin_xyreg<1, 0>(F, KF, fi, fj, t0, d0, w0, n0);
-        o[2 * C.NT] = galerkin_xyreg<-1, 1>(F, KF, fi, fj, t0, d0, w0, n0);
-        o[3 * C.NT] = galerkin_xyreg<0, 1>(F, KF, fi, fj, t0, d0, w0, n0);
-        o[4 * C.NT] = galerkin_xyreg<1, 1>(F, KF, fi, fj, t0, d0, w0, n0);
-        o[5 * C.NT] = galerkin_xyreg<-1, -1>(F, KF, fi, fj, t1, d1, w1, n1);
-        o[6 * C.NT] = galerkin_xyreg<0, -1>(F, KF, fi, fj, t1, d1, w1, n1);
-        o[7 * C.NT] = galerkin_xyreg<1, -1>(F, KF, fi, fj, t1, d1, w1, n1);
-        o[8 * C.NT] = galerkin_xyreg<-1, 0>(F, KF, fi, fj, t1, d1, w1, n1);
-        o[9 * C.NT] = galerkin_xyreg<0, 0>(F, KF, fi, fj, t1, d1, w1, n1);
-        o[10 * C.NT] = galerkin_xyreg<1, 0>(F, KF, fi, fj, t1, d1, w1, n1);
-        o[11 * C.NT] = galerkin_xyreg<-1, 1>(F, KF, fi, fj, t1, d1, w1, n1);
-        o[12 * C.NT] = galerkin_xyreg<0, 1>(F, KF, fi, fj, t1, d1, w1, n1);
-        o[13 * C.NT] = galerkin_xyreg<1, 1>(F, KF, fi, fj, t1, d1, w1, n1);
+        o[0 * C.NT] = galerkin_xyreg<0, 0>(F, KF, fi, fj, z0);
+        o[1 * C.NT] = galerkin_xyreg<1, 0>(F, KF, fi, fj, z0);
+        o[2 * C.NT] = galerkin_xyreg<-1, 1>(F, KF, fi, fj, z0);
+        o[3 * C.NT] = galerkin_xyreg<0, 1>(F, KF, fi, fj, z0);
+        o[4 * C.NT] = galerkin_xyreg<1, 1>(F, KF, fi, fj, z0);
+        o[5 * C.NT] = galerkin_xyreg<-1, -1>(F, KF, fi, fj, z1);
+        o[6 * C.NT] = galerkin_xyreg<0, -1>(F, KF, fi, fj, z1);
+        o[7 * C.NT] = galerkin_xyreg<1, -1>(F, KF, fi, fj, z1);
+        o[8 * C.NT] = galerkin_xyreg<-1, 0>(F, KF, fi, fj, z1);
+        o[9 * C.NT] = galerkin_xyreg<0, 0>(F, KF, fi, fj, z1);
+        o[10 * C.NT] = galerkin_xyreg<1, 0>(F, KF, fi, fj, z1);
+        o[11 * C.NT] = galerkin_xyreg<-1, 1>(F, KF, fi, fj, z1);
+        o[12 * C.NT] = galerkin_xyreg<0, 1>(F, KF, fi, fj, z1);
+        o[13 * C.NT] = galerkin_xyreg<1, 1>(F, KF, fi, fj, z1);
         return;
     }
     if (xyreg) {   // identity z
@@ -812,7 +838,8 @@ void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const d
                      double* coefC, int zident, cudaStream_t st) {
     dim3 grid((Cl.n1 + 127) / 128, Cl.n2, Cl.n3);
     g_launches += 1;
-    galerkin_kernel<<<grid, 128, 0, st>>>(F, Cl, M, coefF, coefC, zident, !g_galerkin_generic);
+    if (zident) galerkin_kernel<true><<<grid, 128, 0, st>>>(F, Cl, M, coefF, coefC, !g_galerkin_generic);
+    else galerkin_kernel<false><<<grid, 128, 0, st>>>(F, Cl, M, coefF, coefC, !g_galerkin_generic);
 }
 
 void launch_export27(const LevDev& L, const double* coef, double* K27, cudaStream_t st) {
