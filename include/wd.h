@@ -112,6 +112,13 @@ typedef struct {
                                 profile off); same iterates, history and cycle count as the
                                 host-driven loop.  Default 0 (host loop): measured no faster
                                 (scripts/device_loop_timing.py, profiles/r2_device_loop.jsonl) */
+    int overlap_halo;        /* slabs (nranks > 1): each fused sweep on a distributed level runs
+                                the tile rows holding the first / last 2 owned rows first and
+                                exchanges those rows on a second stream while the interior tiles
+                                run (boundary-first); results identical to 0.  Default 0: with
+                                virtual ranks on one GPU it measured slower (the boundary launch
+                                runs one tile row per CTA on part of the SMs); untested on
+                                several GPUs (profiles/r2_virtual_ranks.jsonl) */
 } wd_options;
 
 typedef struct {

@@ -40,7 +40,7 @@ class wd_options(C.Structure):
                 ("gather_below_nodes", C.c_longlong), ("rank", C.c_int), ("nranks", C.c_int),
                 ("nccl_comm", C.c_void_p), ("j_begin", C.c_int), ("j_end", C.c_int),
                 ("profile", C.c_int), ("smoother", C.c_int), ("line_from_level", C.c_int),
-                ("device_loop", C.c_int)]
+                ("device_loop", C.c_int), ("overlap_halo", C.c_int)]
 
 
 class wd_report(C.Structure):

@@ -527,9 +527,19 @@ int gs_fused2_prepare() {
 
 // one sweep lin -> lout (k_gs_fused.cu launch_gs_fused); ring_map /
 // ring_map_res: the make_ring_map tensor maps of lin (plain / residual tiles)
+// tile rows of a plain sweep: [0, b0) hold the first w owned rows, [b1, nty)
+// the last w (the rows a slab's neighbours need after the sweep); b0 >= b1
+// means the boundary tiles cover everything
+void gs_fused2_tile_rows(const LevDev& L, int w, int* b0, int* b1, int* nty) {
+    const int jt0 = L.own0 - ((L.own0 + L.jg0) & 1);
+    *nty = (L.own1 - jt0 + TJ_SWEEP - 1) / TJ_SWEEP;
+    *b0 = std::min((L.own0 + w - 1 - jt0) / TJ_SWEEP + 1, *nty);
+    *b1 = std::max((L.own1 - w - jt0) / TJ_SWEEP, 0);
+}
+
 int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
                      const void* ring_map_res, double* lout, const double* f, cudaStream_t st,
-                     double* partial, const ProlongIn* pro) {
+                     double* partial, const ProlongIn* pro, int tr0, int tr1) {
     const int nsm = gs_fused2_prepare();
     KBase KB;
     for (int s = 0; s < 14; s++) {
@@ -538,9 +548,15 @@ int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
         // backward neighbour p - d_s: row j - dy, plane z - dz (x shift per thread)
         KB.kb[s] = coef + (i64)s * L.NT - (i64)dy * L.sj - (i64)dz * L.sk;
     }
-    const int jt0 = L.own0 - ((L.own0 + L.jg0) & 1);
     const int tj = partial ? TJ_RES : TJ_SWEEP;
-    const int ntx = (L.n1 + TI - 1) / TI, nty = (L.own1 - jt0 + tj - 1) / tj;
+    int jt0 = L.own0 - ((L.own0 + L.jg0) & 1);
+    const int ntx = (L.n1 + TI - 1) / TI;
+    int nty = (L.own1 - jt0 + tj - 1) / tj;
+    if (tr1 >= 0 && !partial) {   // tile rows [tr0, tr1) of the plain / PRO sweep
+        jt0 += tr0 * tj;
+        nty = std::max(std::min(tr1, nty) - tr0, 0);
+        if (nty == 0) return 0;
+    }
     g_launches += 1;
     // persistent CTAs; tests may cap their number (env WD_TEST_GS_GRID) so that
     // other tiles share a CTA's cross-tile pipeline

@@ -264,6 +264,13 @@ struct wd_ctx {
     double* dscal = nullptr;   // device scalars
     double* hscal = nullptr;   // pinned host scalars
     cudaStream_t cap = nullptr;
+    // slabs: the halo exchange after a sweep's boundary tiles runs on `side`
+    // while the interior tiles run (boundary-first overlap); halo_fresh[l]:
+    // level l's iterate already has its 2 halo rows current (host-side state
+    // of the launch sequence; reset at every entry point and capture)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool halo_fresh[MAXLEV] = {};
     // host-pointer pipelining (copy-in / compute + copy-out streams, chunk events)
     cudaStream_t pin_s = nullptr, pout_s = nullptr;
     cudaEvent_t pev[17] = {};
@@ -682,11 +689,12 @@ bool v2_level(const Level& F) {
     return g_gs_v2 && F.L.NT < (1ll << 31) && (F.lam == F.raw[1] || F.lam == F.raw[4]);
 }
 int gs_sweep_level(Level& F, cudaStream_t st, double* partial = nullptr,
-                   const ProlongIn* pro = nullptr) {
+                   const ProlongIn* pro = nullptr, int tr0 = 0, int tr1 = -1) {
     if (v2_level(F))
     {
         const int b = F.lam == F.raw[1] ? 0 : 1;
-        return launch_gs_fused2(F.L, F.coef, F.tmR[b], F.tmRr[b], F.lam2, F.f, st, partial, pro);
+        return launch_gs_fused2(F.L, F.coef, F.tmR[b], F.tmRr[b], F.lam2, F.f, st, partial, pro,
+                                tr0, tr1);
     }
     return launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st, partial);
 }
@@ -708,10 +716,11 @@ LevDev target(const Level& lv) {
 }
 
 // ------------------------------------------------------------------ transport
-enum { ARR_LAM = 0, ARR_R = 1, ARR_COEF = 2, ARR_F = 3 };
+enum { ARR_LAM = 0, ARR_R = 1, ARR_COEF = 2, ARR_F = 3, ARR_LAM2 = 4 };
 
 double* arr_of(Level& lv, int which) {
-    return which == ARR_LAM ? lv.lam : which == ARR_R ? lv.r : which == ARR_F ? lv.f : lv.coef;
+    return which == ARR_LAM ? lv.lam : which == ARR_LAM2 ? lv.lam2 : which == ARR_R ? lv.r
+         : which == ARR_F ? lv.f : lv.coef;
 }
 
 // Halo exchange of w rows each side on a distributed level: a part's first w
@@ -838,9 +847,12 @@ struct RoleGuard {
 };
 
 // installs a context's knobs (wd_ctx::knob) in the launchers' globals
+// (and marks every level's halo rows as not known to be current: the caller
+// may have changed the arrays)
 struct KnobScope {
-    explicit KnobScope(const wd_ctx* c) {
+    explicit KnobScope(wd_ctx* c) {
         if (!c) return;
+        for (bool& b : c->halo_fresh) b = false;
         g_gs_v2 = c->knob[0];
         g_test_jitter = c->knob[1];
         g_test_gs_grid = c->knob[2];
@@ -886,10 +898,50 @@ bool fused_level(const wd_ctx* ctx, int l) {
 //  * phased / line relaxation: 4 colour phases in place; on slabs the boundary
 //    rows are exchanged after phase 1 (even rows final) and phase 3 (odd rows
 //    final)
+// boundary-first: may level l's sweeps run their boundary tile rows first and
+// exchange the new boundary rows while the interior tiles run?  Slabs
+// (virtual or NCCL ranks) on a distributed level with the TMA fused sweep
+bool overlap_level(const wd_ctx* ctx, int l) {
+    if (!ctx->opt.overlap_halo || ctx->mode == MODE_SINGLE || !ctx->side) return false;
+    if (!ctx->parts[0].lev[l].dist || !fused_level(ctx, l)) return false;
+    for (const Part& P : ctx->parts)
+        if (!v2_level(P.lev[l])) return false;
+    return true;
+}
+
 int smooth(wd_ctx* ctx, int l, bool prof, int ns, cudaStream_t st, const ProlongIn* pro) {
     if (prof && ns < 16) CK(cudaEventRecordWithFlags(ctx->ev_gs[2 * ns], st, cudaEventRecordExternal));
-    if (fused_level(ctx, l)) {
-        RC(exchange(ctx, l, ARR_LAM, 2, st));
+    const bool fresh = ctx->halo_fresh[l];
+    ctx->halo_fresh[l] = false;
+    if (fused_level(ctx, l) && overlap_level(ctx, l) && !pro) {
+        // the input's halo rows, unless the previous sweep's overlapped exchange
+        // already brought them; then the tile rows holding the first / last 2
+        // owned rows, the exchange of those rows of the output on the side
+        // stream, the interior tile rows meanwhile (any tiling gives the same
+        // node updates: the tiles recompute their halos)
+        if (!fresh) RC(exchange(ctx, l, ARR_LAM, 2, st));
+        std::vector<int> b0(ctx->parts.size()), b1(ctx->parts.size()), nty(ctx->parts.size());
+        for (size_t p = 0; p < ctx->parts.size(); p++) {
+            Level& F = ctx->parts[p].lev[l];
+            gs_fused2_tile_rows(F.L, 2, &b0[p], &b1[p], &nty[p]);
+            if (b0[p] >= b1[p]) {   // no interior: all tile rows now
+                gs_sweep_level(F, st);
+            } else {
+                gs_sweep_level(F, st, nullptr, nullptr, 0, b0[p]);
+                gs_sweep_level(F, st, nullptr, nullptr, b1[p], nty[p]);
+            }
+        }
+        CK(cudaEventRecord(ctx->ev_fork, st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        RC(exchange(ctx, l, ARR_LAM2, 2, ctx->side));
+        for (size_t p = 0; p < ctx->parts.size(); p++)
+            if (b0[p] < b1[p]) gs_sweep_level(ctx->parts[p].lev[l], st, nullptr, nullptr, b0[p], b1[p]);
+        CK(cudaEventRecord(ctx->ev_join, ctx->side));
+        CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+        for (Part& P : ctx->parts) std::swap(P.lev[l].lam, P.lev[l].lam2);
+        ctx->halo_fresh[l] = true;
+    } else if (fused_level(ctx, l)) {
+        if (!fresh) RC(exchange(ctx, l, ARR_LAM, 2, st));
         for (Part& P : ctx->parts) {
             Level& F = P.lev[l];
             gs_sweep_level(F, st, nullptr, pro);
@@ -921,7 +973,7 @@ int smooth_end(wd_ctx* ctx, int l, cudaStream_t st) {
             F.lam = F.raw[1];
         }
     }
-    if (fused_level(ctx, l)) RC(exchange(ctx, l, ARR_LAM, 1, st));
+    if (fused_level(ctx, l) && !ctx->halo_fresh[l]) RC(exchange(ctx, l, ARR_LAM, 1, st));
     return WD_OK;
 }
 
@@ -931,6 +983,7 @@ int smooth_end(wd_ctx* ctx, int l, cudaStream_t st) {
 int smooth_first_res(wd_ctx* ctx, bool prof, cudaStream_t st) {
     if (prof) CK(cudaEventRecordWithFlags(ctx->ev_gs[0], st, cudaEventRecordExternal));
     RC(exchange(ctx, 0, ARR_LAM, 2, st));
+    ctx->halo_fresh[0] = false;
     double* per = ctx->dscal + 128;   // per-part sums
     for (size_t p = 0; p < ctx->parts.size(); p++) {
         Part& P = ctx->parts[p];
@@ -992,6 +1045,7 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st, int first = 0) {
     if (l + 1 == ctx->gather) RC(gather_rows(ctx, l + 1, ARR_F, st));
     else if (fused_level(ctx, l + 1)) RC(exchange(ctx, l + 1, ARR_F, 1, st));   // halo row of f_c
     for (Part& P : ctx->parts) CK(cudaMemsetAsync(P.lev[l + 1].lam, 0, sizeof(double) * P.lev[l + 1].L.NT, st));
+    ctx->halo_fresh[l + 1] = false;
     CKL();
     n_res.end();
     RC(vcycle_level(ctx, l + 1, st));
@@ -1006,6 +1060,7 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st, int first = 0) {
         pro.w = ctx->corr_w;
     } else {
         Nvtx n_pro("prolongation");
+        ctx->halo_fresh[l] = false;
         for (Part& P : ctx->parts) {
             Level& F = P.lev[l];
             Level& C = P.lev[l + 1];
@@ -1461,6 +1516,7 @@ void wd_default_options(wd_options* o) {
     o->smoother = WD_SMOOTH_FUSED;
     o->line_from_level = -1;
     o->device_loop = 0;
+    o->overlap_halo = 0;
 }
 
 const char* wd_last_error(void) { return g_err; }
@@ -1475,6 +1531,9 @@ void wd_destroy(wd_ctx* ctx) {
     dfree(ctx->loopd);
     if (ctx->looph) cudaFreeHost(ctx->looph);
     if (ctx->cap) cudaStreamDestroy(ctx->cap);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->pin_s) cudaStreamDestroy(ctx->pin_s);
     if (ctx->pout_s) cudaStreamDestroy(ctx->pout_s);
     for (auto e : ctx->pev) if (e) cudaEventDestroy(e);
@@ -1673,6 +1732,11 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
     RC(dalloc(ctx, (void**)&ctx->dscal, sizeof(double) * 4096));
     CK(cudaMallocHost((void**)&ctx->hscal, sizeof(double) * 64));
     CK(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
+    if (ctx->mode != MODE_SINGLE) {
+        CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+    }
     apply_tma_prepare();
     gs_fused_prepare();
     gs_fused2_prepare();

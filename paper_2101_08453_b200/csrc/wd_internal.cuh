@@ -169,9 +169,12 @@ struct ProlongIn {
 };
 // ring_map / ring_map_res: make_ring_map(.., res = false / true) of lin (the
 // plain / PRO sweeps tile 64 x 8, the residual variant (partial) 64 x 6)
+// tr0, tr1: only the tile rows [tr0, tr1) (plain / PRO sweeps; tr1 < 0: all)
 int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
                      const void* ring_map_res, double* lout, const double* f, cudaStream_t st,
-                     double* partial = nullptr, const ProlongIn* pro = nullptr);
+                     double* partial = nullptr, const ProlongIn* pro = nullptr, int tr0 = 0,
+                     int tr1 = -1);
+void gs_fused2_tile_rows(const LevDev& L, int w, int* b0, int* b1, int* nty);
 
 // k_io.cu: steps either side of the path
 void launch_build_mesh(const double* zs, int n1, int n2, int n3, double x0, double y0, double dx,

@@ -25,14 +25,17 @@ def main():
     ap.add_argument("--config", default="paper")
     ap.add_argument("--ranks", default="1,2,4,8")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--overlap", default="1", help="wd_options.overlap_halo values to run, e.g. 0,1")
     args = ap.parse_args()
     import paper_2101_08453_b200 as wd
     import synth
     dev = torch.device("cuda:0")
     p = synth.make(args.config, device=dev)
     ref = None
-    for R in [int(r) for r in args.ranks.split(",")]:
-        opt = wd.default_options(profile=1, nranks=R, rank=-1 if R > 1 else 0)
+    runs = [(int(r), int(o)) for r in args.ranks.split(",") for o in args.overlap.split(",")
+            if int(r) > 1 or o == args.overlap.split(",")[0]]
+    for R, ov in runs:
+        opt = wd.default_options(profile=1, nranks=R, rank=-1 if R > 1 else 0, overlap_halo=ov)
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ctx = wd.wd_assemble(p.X, p.Y, p.Z, p.a, opt)   # warm
         f = wd.wd_rhs(ctx, p.u0)
@@ -56,7 +59,7 @@ def main():
                 ref = lam.clone()
             same = bool(torch.equal(lam, ref))
             ctx.close()
-        line = dict(config=args.config, ranks=R, setup_ms=setup / args.reps,
+        line = dict(config=args.config, ranks=R, overlap_halo=ov, setup_ms=setup / args.reps,
                     solve_ms=solve / args.reps, cycles=cyc / args.reps,
                     vcycle_ms=prof["vcycle_ms"] / max(prof["vcycles"], 1),
                     gather_level=gl, lambda_bitwise_equal_to_1_rank=same)

@@ -120,3 +120,52 @@ def test_nccl_one_rank_bitwise(wd):
     assert torch.equal(wd.wd_recover_wind(ref, l1, p.u0), wd.wd_recover_wind(ctx, lN, p.u0))
     ctx.close()
     ref.close()
+
+
+@pytest.mark.parametrize("name", list(PROBLEMS))
+@pytest.mark.parametrize("nranks,use_graph", [(2, 1), (3, 1), (4, 0), (6, 1)])
+def test_boundary_first_overlap_bitwise(wd, name, nranks, use_graph):
+    """Boundary-first sweeps (wd_options.overlap_halo = 1; off by default):
+    each fused sweep on a distributed level runs the tile rows holding the
+    first / last 2 owned rows, exchanges those rows on a second stream while
+    the interior tile rows run, and skips the next sweep's leading exchange.
+    Every V-cycle iterate, the solve and its history equal the serial order
+    (overlap_halo = 0) and one part bit for bit."""
+    p = PROBLEMS[name]()
+
+    def mk(nr, ov):
+        opt = wd.default_options(coarsest_max_free=200, nranks=nr, rank=-1 if nr > 1 else 0,
+                                 gather_below_nodes=1000, overlap_halo=ov, use_graph=use_graph)
+        return wd.wd_assemble(p.X, p.Y, p.Z, p.a, opt)
+
+    ref, ser, ovl = mk(1, 0), mk(nranks, 0), mk(nranks, 1)
+    try:
+        f = wd.wd_rhs(ref, p.u0)
+        lams = [synth.random_lambda(p, 6).to(DEV) for _ in range(3)]
+        for c in range(3):
+            for ctx, lam in zip((ref, ser, ovl), lams):
+                wd.wd_vcycle(ctx, lam, f)
+            assert torch.equal(lams[0], lams[1]) and torch.equal(lams[1], lams[2]), c
+        out = [wd.wd_solve(ctx, f, rel_tol=1e-9) for ctx in (ref, ser, ovl)]
+        assert torch.equal(out[0][0], out[2][0]) and torch.equal(out[1][0], out[2][0])
+        assert out[0][1]["hist"] == out[2][1]["hist"] or all(
+            abs(a - b) <= 1e-12 * b for a, b in zip(out[0][1]["hist"], out[2][1]["hist"]) if b)
+        assert out[1][1]["hist"] == out[2][1]["hist"]
+    finally:
+        for ctx in (ref, ser, ovl):
+            ctx.close()
+    # longer runs of consecutive sweeps (4 pre, 3 post): each reuses the halo
+    # rows the previous sweep's overlapped exchange brought
+    opt = dict(coarsest_max_free=200, nranks=nranks, rank=-1, gather_below_nodes=1000,
+               pre_smooth=4, post_smooth=3, use_graph=use_graph)
+    a = wd.wd_assemble(p.X, p.Y, p.Z, p.a, wd.default_options(overlap_halo=0, **opt))
+    b = wd.wd_assemble(p.X, p.Y, p.Z, p.a, wd.default_options(overlap_halo=1, **opt))
+    try:
+        x1, x2 = synth.random_lambda(p, 8).to(DEV), synth.random_lambda(p, 8).to(DEV)
+        for _ in range(2):
+            wd.wd_vcycle(a, x1, f)
+            wd.wd_vcycle(b, x2, f)
+        assert torch.equal(x1, x2)
+    finally:
+        a.close()
+        b.close()
