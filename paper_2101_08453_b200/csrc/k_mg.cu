@@ -834,6 +834,30 @@ void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const do
     prolong_kernel<<<grid, 128, 0, st>>>(F, Cl, M, xc, x, zident, w);
 }
 
+// The 14 coefficient arrays are allocated without a zero fill; this writes
+// zeros where neither writer does: the padding positions of every half row,
+// and (galerkin) the Dirichlet nodes, which the Galerkin product skips (the
+// assembly writes every real node).  Either writer fills the rest.
+__global__ void zero_unwritten_kernel(LevDev L, double* __restrict__ coef, int galerkin) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;   // position in the row block's plane
+    const int j = blockIdx.y, k = blockIdx.z;
+    if (e >= L.P) return;
+    const int half = e >= L.H, pos = e - half * L.H;
+    const int i = 2 * pos + half;
+    const bool pad = i >= L.n1;
+    const bool dir = i == 0 || i == L.n1 - 1 || row_dirichlet(L, j) || k == L.n3 - 1;
+    if (!pad && !(galerkin && dir)) return;
+    const i64 o = (i64)j * L.sj + (i64)k * L.sk + e;
+#pragma unroll
+    for (int s = 0; s < 14; s++) coef[s * L.NT + o] = 0.0;
+}
+
+void launch_zero_unwritten(const LevDev& L, double* coef, bool galerkin, cudaStream_t st) {
+    dim3 grid((L.P + 127) / 128, L.n2, L.n3);
+    g_launches += 1;
+    zero_unwritten_kernel<<<grid, 128, 0, st>>>(L, coef, galerkin ? 1 : 0);
+}
+
 void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* coefF,
                      double* coefC, int zident, cudaStream_t st) {
     dim3 grid((Cl.n1 + 127) / 128, Cl.n2, Cl.n3);

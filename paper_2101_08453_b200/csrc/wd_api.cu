@@ -332,7 +332,9 @@ void ensure_pool() {
 // Device allocations come from the stream-ordered pool of the device with an
 // unlimited release threshold: a context built after another one was destroyed
 // reuses the retained memory instead of remapping it.
-int dalloc(wd_ctx* ctx, void** p, size_t bytes) {
+// zero = false: the caller overwrites every entry that is ever read (big
+// arrays whose zero-fill would cost a pass over HBM)
+int dalloc(wd_ctx* ctx, void** p, size_t bytes, bool zero = true) {
     ensure_pool();
     const size_t b = bytes > 0 ? bytes : 8;
     cudaError_t e = cudaMallocAsync(p, b, 0);
@@ -342,7 +344,7 @@ int dalloc(wd_ctx* ctx, void** p, size_t bytes) {
                     "cudaMallocAsync(%zu) failed: %s", bytes, cudaGetErrorString(e));
     }
     if (ctx) ctx->bytes += (long long)bytes;
-    e = cudaMemsetAsync(*p, 0, b, 0);
+    if (zero) e = cudaMemsetAsync(*p, 0, b, 0);
     if (e == cudaSuccess) e = cudaStreamSynchronize(0);
     if (e != cudaSuccess) return fail(WD_E_CUDA, "cudaMemset failed: %s", cudaGetErrorString(e));
     return WD_OK;
@@ -663,16 +665,21 @@ std::vector<HaloMsg> halo_msgs(const PartLevel& P, int rank, int nranks, int w) 
     return m;
 }
 
-int alloc_level(wd_ctx* ctx, Level& lv) {
+// galerkin: the coefficients will come from the Galerkin product (free nodes
+// only) rather than the assembly (every node); either way the entries the
+// writer leaves alone are zeroed here instead of zero-filling all 14 arrays
+int alloc_level(wd_ctx* ctx, Level& lv, bool galerkin) {
     const size_t nt = (size_t)lv.L.NT;
     double** arr[5] = {&lv.coef, &lv.lam, &lv.f, &lv.r, &lv.lam2};
     const size_t len[5] = {14 * nt, nt, nt, nt, nt};
     for (int t = 0; t < 5; t++) {
-        RC(dalloc(ctx, (void**)&lv.raw[t], sizeof(double) * len[t]));
+        // the vectors zero-filled (D entries of the ping-pong buffer stay 0:
+        // the fused sweep writes free nodes only)
+        RC(dalloc(ctx, (void**)&lv.raw[t], sizeof(double) * len[t], t != 0));
         *arr[t] = lv.raw[t];
     }
-    // D entries of the ping-pong buffer stay 0 (the fused sweep writes free nodes only)
-    CK(cudaMemset(lv.lam2, 0, sizeof(double) * nt));
+    launch_zero_unwritten(lv.L, lv.coef, galerkin, 0);
+    CK(cudaStreamSynchronize(0));
     if (make_coef_maps(lv.L, lv.coef, lv.tmA, lv.tmB) || make_vec_map(lv.L, lv.lam, lv.tmX, true) ||
         make_vec_map(lv.L, lv.f, lv.tmF, false) || make_ring_map(lv.L, lv.raw[1], lv.tmR[0], false) ||
         make_ring_map(lv.L, lv.raw[4], lv.tmR[1], false) ||
@@ -1694,7 +1701,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
         const size_t n = (size_t)n1 * n2 * n3, plane = (size_t)n1 * n2;
         double** dst[3] = {&P.X, &P.Y, &P.Z};
         const double* src[3] = {X, Y, Z};
-        for (int d = 0; d < 3; d++) RC(dalloc(ctx, (void**)dst[d], sizeof(double) * n));
+        for (int d = 0; d < 3; d++) RC(dalloc(ctx, (void**)dst[d], sizeof(double) * n, false));
         CK(cudaEventRecord(ctx->pev[16], st));
         CK(cudaStreamWaitEvent(ctx->pin_s, ctx->pev[16], 0));
         for (int c = 0; c < NCH; c++) {
@@ -1721,7 +1728,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
             double** dst[3] = {&P.X, &P.Y, &P.Z};
             const double* src[3] = {sx.d, sy.d, sz.d};
             for (int d = 0; d < 3; d++) {
-                RC(dalloc(ctx, (void**)dst[d], sizeof(double) * n));
+                RC(dalloc(ctx, (void**)dst[d], sizeof(double) * n, false));   // copied over
                 CK(cudaMemcpy2DAsync(*dst[d], sizeof(double) * n1 * rows,
                                      src[d] + (size_t)jofs * n1, sizeof(double) * n1 * rows_in,
                                      sizeof(double) * n1 * rows, n3, cudaMemcpyDeviceToDevice, st));
@@ -1760,7 +1767,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
         L0.dist = multi;
         L0.cown0 = L0.L.own0;
         L0.cown1 = L0.L.own1;
-        RC(alloc_level(ctx, L0));
+        RC(alloc_level(ctx, L0, false));
         CK(cudaMemsetAsync(dbad, 0xff, sizeof(unsigned long long), st));
         if (piped) {
             // tile rows whose node rows have all arrived, chunk by chunk
@@ -1941,7 +1948,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
             C.cown0 = pc.cown0;
             C.cown1 = pc.cown1;
             const int jlo_c = C.L.jg0;
-            RC(alloc_level(ctx, C));
+            RC(alloc_level(ctx, C, true));
             // maps: x and z global; y local to the part (fine rows F.jg0.., coarse rows jlo_c..)
             const int fr = F.L.n2, cr = C.L.n2;
             std::vector<int> glo(fn2), gco(fn2), xlo(fn1), xco(fn1), zlo(fn3), zco(fn3);

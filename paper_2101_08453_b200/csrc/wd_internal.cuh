@@ -140,6 +140,9 @@ void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const do
                     double* x, int zident, cudaStream_t st, double w = 1.0);
 // zident: the z map of this transition is the identity (no layer merged);
 // regular interior columns then take an unrolled path (bitwise equal)
+// zeros at the coefficient entries neither the assembly nor (galerkin) the
+// Galerkin product writes: half-row padding, and Dirichlet nodes when galerkin
+void launch_zero_unwritten(const LevDev& L, double* coef, bool galerkin, cudaStream_t st);
 void launch_galerkin(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* coefF,
                      double* coefC, int zident, cudaStream_t st);
 void launch_export27(const LevDev& L, const double* coef, double* K27, cudaStream_t st);
