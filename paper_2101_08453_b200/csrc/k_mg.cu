@@ -347,12 +347,57 @@ __device__ __forceinline__ int support1d(const int* __restrict__ pos, const int*
     return m;
 }
 
+// ZID: the transition's z map is the identity; the merging instance keeps
+// the z supports of every coarse plane in shared memory (once per CTA), the
+// identity one no shared memory (its L1 serves the 3 x 3 neighbourhoods)
+template <bool ZID>
 __global__ void __launch_bounds__(128)
 restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
-                double* __restrict__ fc, int zident) {
+                double* __restrict__ fc) {
+    constexpr bool zident = ZID;
     const int I = blockIdx.x * 128 + threadIdx.x;
     const int J = blockIdx.y;
+    constexpr int ZMAX = ZID ? 1 : 128;
+    __shared__ int zt[ZMAX][3];
+    __shared__ double zw[ZMAX][3];
+    __shared__ int zm[ZMAX];
+    const bool ztab = !ZID && C.n3 - 1 <= ZMAX;
+    if (ztab) {
+        for (int Kc = threadIdx.x; Kc <= C.n3 - 2; Kc += 128) {
+            int t[3];
+            double w[3];
+            zm[Kc] = support1d(M.pos[2], M.co[2], F.n3, Kc, t, w);
+            for (int c = 0; c < 3; c++) {
+                zt[Kc][c] = t[c];
+                zw[Kc][c] = w[c];
+            }
+        }
+        __syncthreads();
+    }
     if (I < 1 || I > C.n1 - 2 || !row_free(C, J)) return;
+    if (ztab && regular1d(M.pos[0], C.n1, I) && regular1d(M.pos[1], C.n2, J)) {
+        // regular x and y supports {-1, 0, 1}, weights (1/2, 1, 1/2), z from the
+        // table: the generic loop below with x and y unrolled (bitwise equal)
+        const double w[3] = {0.5, 1.0, 0.5};
+        const int fi = M.pos[0][I], fj = M.pos[1][J];
+        for (int Kc = 0; Kc <= C.n3 - 2; Kc++) {
+            const int mz = zm[Kc];
+            double s = 0.0;
+            for (int c = 0; c < mz; c++) {
+                const int kz = zt[Kc][c];
+                const double wzc = zw[Kc][c];
+#pragma unroll
+                for (int b = 0; b < 3; b++) {
+                    double sr = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 3; a++) sr = fma(w[a], ldg(r + loff(F, fi + a - 1, fj + b - 1, kz)), sr);
+                    s = fma(wzc * w[b], sr, s);
+                }
+            }
+            fc[loff(C, I, J, Kc)] = s;
+        }
+        return;
+    }
     if (zident && regular1d(M.pos[0], C.n1, I) && regular1d(M.pos[1], C.n2, J)) {
         // regular supports {-1, 0, 1} x {-1, 0, 1}, weights (1/2, 1, 1/2), identity in z:
         // the generic loop below with compile-time weights (same order, bitwise equal)
@@ -392,11 +437,26 @@ restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
     }
 }
 
+// ZTAB: the merging instance, which tables every fine plane's z parent and
+// count in shared memory; the identity-z instance keeps zident a run-time
+// flag (as a compile-time constant the compiler batches the plane loop's
+// loads at 120 registers: level-0 prolongation 0.67 -> 1.56 ms)
+template <bool ZTAB>
 __global__ void __launch_bounds__(128)
 prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
                double* __restrict__ x, int zident, double w) {
     const int i = blockIdx.x * 128 + threadIdx.x;
     const int j = blockIdx.y;
+    constexpr int ZMAX = ZTAB ? 256 : 1;
+    __shared__ int zl[ZMAX], zn[ZMAX];
+    const bool ztab = ZTAB && !zident && F.n3 - 1 <= ZMAX;
+    if (ztab) {
+        for (int k = threadIdx.x; k <= F.n3 - 2; k += 128) {
+            zl[k] = M.lo[2][k];
+            zn[k] = M.co[2][k] ? 1 : 2;
+        }
+        __syncthreads();
+    }
     if (i < 1 || i > F.n1 - 2 || !row_free(F, j)) return;
     const int ix = M.lo[0][i], iy = M.lo[1][j];
     const int nx = M.co[0][i] ? 1 : 2, ny = M.co[1][j] ? 1 : 2;
@@ -427,6 +487,35 @@ prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
             }
             // x + w s: with w = 1 (Eq. (7)) the product is exact, so this is
             // x + s bit for bit; w != 1 only for the divergence-guard test
+            xo[(i64)k * F.sk] = fma(w, s, xo[(i64)k * F.sk]);
+        }
+        return;
+    }
+    if (ztab) {
+        // the generic loop below with x branch-free (as the identity-z path)
+        // and z from the table (bitwise equal)
+        const double* c0 = xc + loff(C, ix, iy, 0);
+        const double* c1 = xc + loff(C, ix + nx - 1, iy, 0);
+        const double* c2 = xc + loff(C, ix, iy + ny - 1, 0);
+        const double* c3 = xc + loff(C, ix + nx - 1, iy + ny - 1, 0);
+        double* xo = x + loff(F, i, j, 0);
+        const bool two = nx == 2;
+#pragma unroll 4
+        for (int k = 0; k <= F.n3 - 2; k++) {
+            const int iz = zl[k], nz = zn[k];
+            const double wz = nz == 1 ? 1.0 : 0.5;
+            double s = 0.0;
+            for (int c = 0; c < nz; c++) {
+                const i64 kc = (i64)(iz + c) * C.sk;
+                double sr = 0.0 + ldg(c0 + kc);
+                sr += two ? ldg(c1 + kc) : -0.0;
+                s = fma(wy * wz, wx * sr, s);
+                if (ny == 2) {
+                    double sr2 = 0.0 + ldg(c2 + kc);
+                    sr2 += two ? ldg(c3 + kc) : -0.0;
+                    s = fma(wy * wz, wx * sr2, s);
+                }
+            }
             xo[(i64)k * F.sk] = fma(w, s, xo[(i64)k * F.sk]);
         }
         return;
@@ -824,14 +913,16 @@ void launch_restrict(const LevDev& F, const LevDev& Cl, const MapDev& M, const d
                      double* fc, int zident, cudaStream_t st) {
     dim3 grid((Cl.n1 + 127) / 128, Cl.n2);
     g_launches += 1;
-    restrict_kernel<<<grid, 128, 0, st>>>(F, Cl, M, r, fc, zident);
+    if (zident) restrict_kernel<true><<<grid, 128, 0, st>>>(F, Cl, M, r, fc);
+    else restrict_kernel<false><<<grid, 128, 0, st>>>(F, Cl, M, r, fc);
 }
 
 void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* xc,
                     double* x, int zident, cudaStream_t st, double w) {
     dim3 grid((F.n1 + 127) / 128, F.n2);
     g_launches += 1;
-    prolong_kernel<<<grid, 128, 0, st>>>(F, Cl, M, xc, x, zident, w);
+    if (zident) prolong_kernel<false><<<grid, 128, 0, st>>>(F, Cl, M, xc, x, 1, w);
+    else prolong_kernel<true><<<grid, 128, 0, st>>>(F, Cl, M, xc, x, 0, w);
 }
 
 // The 14 coefficient arrays are allocated without a zero fill; this writes
