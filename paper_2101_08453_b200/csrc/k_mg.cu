@@ -375,12 +375,15 @@ restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
         __syncthreads();
     }
     if (I < 1 || I > C.n1 - 2 || !row_free(C, J)) return;
+    // coarse planes of this thread: all, or (small levels, gridDim.z > 1) one
+    const int kz0 = gridDim.z > 1 ? (int)blockIdx.z : 0;
+    const int kz1 = gridDim.z > 1 ? min(kz0 + 1, C.n3 - 1) : C.n3 - 1;
     if (ztab && regular1d(M.pos[0], C.n1, I) && regular1d(M.pos[1], C.n2, J)) {
         // regular x and y supports {-1, 0, 1}, weights (1/2, 1, 1/2), z from the
         // table: the generic loop below with x and y unrolled (bitwise equal)
         const double w[3] = {0.5, 1.0, 0.5};
         const int fi = M.pos[0][I], fj = M.pos[1][J];
-        for (int Kc = 0; Kc <= C.n3 - 2; Kc++) {
+        for (int Kc = kz0; Kc < kz1; Kc++) {
             const int mz = zm[Kc];
             double s = 0.0;
             for (int c = 0; c < mz; c++) {
@@ -404,7 +407,7 @@ restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
         const double w[3] = {0.5, 1.0, 0.5};
         const int fi = M.pos[0][I], fj = M.pos[1][J];
 #pragma unroll 5   // several planes' 9 loads in flight
-        for (int Kc = 0; Kc <= C.n3 - 2; Kc++) {
+        for (int Kc = kz0; Kc < kz1; Kc++) {
             double s = 0.0;
 #pragma unroll
             for (int b = 0; b < 3; b++) {
@@ -422,7 +425,7 @@ restrict_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ r,
     const int mx = support1d(M.pos[0], M.co[0], F.n1, I, tx, wx);
     const int my = support1d(M.pos[1], M.co[1], F.n2, J, ty, wy);
 #pragma unroll 4
-    for (int Kc = 0; Kc <= C.n3 - 2; Kc++) {
+    for (int Kc = kz0; Kc < kz1; Kc++) {
         int tz[3];
         double wz[3];
         const int mz = support1d(M.pos[2], M.co[2], F.n3, Kc, tz, wz);
@@ -458,6 +461,9 @@ prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
         __syncthreads();
     }
     if (i < 1 || i > F.n1 - 2 || !row_free(F, j)) return;
+    // fine planes of this thread: all, or (small levels, gridDim.z > 1) one
+    const int kz0 = gridDim.z > 1 ? (int)blockIdx.z : 0;
+    const int kz1 = gridDim.z > 1 ? min(kz0 + 1, F.n3 - 1) : F.n3 - 1;
     const int ix = M.lo[0][i], iy = M.lo[1][j];
     const int nx = M.co[0][i] ? 1 : 2, ny = M.co[1][j] ? 1 : 2;
     const double wx = nx == 1 ? 1.0 : 0.5, wy = ny == 1 ? 1.0 : 0.5;
@@ -475,7 +481,7 @@ prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
 // ahead of the stores, and a memory-order (row block) variant, all measured
 // slower at Paper-scale level 0 (0.73 / 0.93 / 1.26 / 0.79 ms against 0.66)
 #pragma unroll 16
-        for (int k = 0; k <= F.n3 - 2; k++) {
+        for (int k = kz0; k < kz1; k++) {
             const i64 kc = (i64)k * C.sk;
             double sr = 0.0 + ldg(c0 + kc);
             sr += two ? ldg(c1 + kc) : -0.0;
@@ -501,7 +507,7 @@ prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
         double* xo = x + loff(F, i, j, 0);
         const bool two = nx == 2;
 #pragma unroll 4
-        for (int k = 0; k <= F.n3 - 2; k++) {
+        for (int k = kz0; k < kz1; k++) {
             const int iz = zl[k], nz = zn[k];
             const double wz = nz == 1 ? 1.0 : 0.5;
             double s = 0.0;
@@ -521,7 +527,7 @@ prolong_kernel(LevDev F, LevDev C, MapDev M, const double* __restrict__ xc,
         return;
     }
 #pragma unroll 4
-    for (int k = 0; k <= F.n3 - 2; k++) {
+    for (int k = kz0; k < kz1; k++) {
         const int iz = M.lo[2][k];
         const int nz = M.co[2][k] ? 1 : 2;
         const double wz = nz == 1 ? 1.0 : 0.5;
@@ -909,9 +915,17 @@ void launch_norm2_partial(const LevDev& L, const double* v, double* partial, int
     *nblk = nb;
 }
 
+#ifndef WD_SMALL_COLS
+#define WD_SMALL_COLS (300LL * 300LL)
+#endif
+constexpr long long SMALL_COLS = WD_SMALL_COLS;
+
 void launch_restrict(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* r,
                      double* fc, int zident, cudaStream_t st) {
-    dim3 grid((Cl.n1 + 127) / 128, Cl.n2);
+    // small levels: one coarse plane per CTA layer (the per-thread plane loop
+    // is latency-bound there)
+    const bool split = (long long)Cl.n1 * Cl.n2 <= SMALL_COLS;
+    dim3 grid((Cl.n1 + 127) / 128, Cl.n2, split ? Cl.n3 - 1 : 1);
     g_launches += 1;
     if (zident) restrict_kernel<true><<<grid, 128, 0, st>>>(F, Cl, M, r, fc);
     else restrict_kernel<false><<<grid, 128, 0, st>>>(F, Cl, M, r, fc);
@@ -919,7 +933,8 @@ void launch_restrict(const LevDev& F, const LevDev& Cl, const MapDev& M, const d
 
 void launch_prolong(const LevDev& F, const LevDev& Cl, const MapDev& M, const double* xc,
                     double* x, int zident, cudaStream_t st, double w) {
-    dim3 grid((F.n1 + 127) / 128, F.n2);
+    const bool split = (long long)F.n1 * F.n2 <= SMALL_COLS;
+    dim3 grid((F.n1 + 127) / 128, F.n2, split ? F.n3 - 1 : 1);
     g_launches += 1;
     if (zident) prolong_kernel<false><<<grid, 128, 0, st>>>(F, Cl, M, xc, x, 1, w);
     else prolong_kernel<true><<<grid, 128, 0, st>>>(F, Cl, M, xc, x, 0, w);
