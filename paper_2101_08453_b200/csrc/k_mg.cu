@@ -240,6 +240,8 @@ apply_kernel(LevDev L, const double* __restrict__ K, const double* __restrict__ 
         a = blockIdx.x * 128 + threadIdx.x; ci = blockIdx.z; j = blockIdx.y;
     } else if (variant == 1) {   // 128 along the half row, parity interleaved in blockIdx.x
         a = (blockIdx.x >> 1) * 128 + threadIdx.x; ci = blockIdx.x & 1; j = blockIdx.y;
+    } else if (variant == 4) {   // as 1, one plane per CTA layer (blockIdx.z; small levels)
+        a = (blockIdx.x >> 1) * 128 + threadIdx.x; ci = blockIdx.x & 1; j = blockIdx.y;
     } else if (variant == 2) {   // 32 x 2 parities x AP_ROWS rows
         a = blockIdx.x * 32 + threadIdx.x; ci = threadIdx.y; j = blockIdx.y * AP_ROWS + threadIdx.z;
     } else {                     // 128 x 2 parities, one row
@@ -251,14 +253,17 @@ apply_kernel(LevDev L, const double* __restrict__ K, const double* __restrict__ 
         i64 co[9];
         column_offsets(L, ci, co);
         const i64 own = loff(L, i, j, 0);
+        const int kz0 = variant == 4 ? (int)blockIdx.z : 0;
+        const int kz1 = variant == 4 ? kz0 + 1 : L.n3 - 1;
+        const i64 o0 = own + (i64)kz0 * L.sk;
         double xm[9], x0[9], xp[9];
 #pragma unroll
         for (int c = 0; c < 9; c++) {
-            xm[c] = 0.0;
-            x0[c] = ldg(x + own + co[c]);
-            xp[c] = ldg(x + own + L.sk + co[c]);
+            xm[c] = kz0 > 0 ? ldg(x + o0 - L.sk + co[c]) : 0.0;
+            x0[c] = ldg(x + o0 + co[c]);
+            xp[c] = ldg(x + o0 + L.sk + co[c]);
         }
-        for (int k = 0; k <= L.n3 - 2; k++) {
+        for (int k = kz0; k < kz1; k++) {
             const i64 base = own + (i64)k * L.sk;
             double s = offdiag(L, K, base, co, xm, x0, xp, k > 0);
             s = fma(ldg(K + base), x0[4], s);
@@ -280,7 +285,8 @@ apply_kernel(LevDev L, const double* __restrict__ K, const double* __restrict__ 
     if (partial) {
         const double s = block_sum(acc);
         if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0)
-            partial[(i64)blockIdx.y * gridDim.x + blockIdx.x] = s;
+            partial[((i64)(variant == 4 ? blockIdx.z : 0) * gridDim.y + blockIdx.y) * gridDim.x +
+                    blockIdx.x] = s;
     }
 }
 
@@ -889,13 +895,14 @@ void launch_sum_ordered(const double* v, int n, double* out, cudaStream_t st) {
 }
 
 int launch_apply(const LevDev& L, const double* coef, const double* x, const double* f, double* y,
-                 double* partial, cudaStream_t st) {
+                 double* partial, cudaStream_t st, int variant) {
     const int half = (L.n1 + 1) / 2;
-    const int v = g_apply_variant;
+    const int v = variant >= 0 ? variant : g_apply_variant;
     dim3 grid, blk;
     if (v == 0) { grid = dim3((half + 127) / 128, L.n2, 2); blk = dim3(128); }
     else if (v == 1) { grid = dim3(2 * ((half + 127) / 128), L.n2, 1); blk = dim3(128); }
     else if (v == 2) { grid = dim3((half + 31) / 32, (L.n2 + AP_ROWS - 1) / AP_ROWS, 1); blk = dim3(32, 2, AP_ROWS); }
+    else if (v == 4) { grid = dim3(2 * ((half + 127) / 128), L.n2, L.n3 - 1); blk = dim3(128); }
     else { grid = dim3((half + 127) / 128, L.n2, 1); blk = dim3(128, 2); }
     g_launches += 1;
     apply_kernel<<<grid, blk, 0, st>>>(L, coef, x, f, y, partial, v);

@@ -708,6 +708,12 @@ int gs_sweep_level(Level& F, cudaStream_t st, double* partial = nullptr,
 
 // residual r = f - K lam (f_on) or r = K lam on level `lv`; optional per-CTA partials
 int apply_level(Level& lv, bool f_on, double* partial, cudaStream_t st) {
+    // small levels: the plane-parallel operator kernel (the TMA kernel's
+    // persistent tiles are latency-bound there).  Decided on the level's global
+    // size, so that every slab and one part take the same kernel (the two sum
+    // the stencil in different orders)
+    if (g_apply_variant >= 0 && (long long)lv.L.n1 * lv.L.n2g <= APPLY_SMALL_COLS)
+        return launch_apply(lv.L, lv.coef, lv.lam, f_on ? lv.f : nullptr, lv.r, partial, st, 4);
     if (g_apply_variant >= 0)
         return launch_apply_tma(lv.L, lv.tmA, lv.tmB, lv.tmX, f_on ? lv.tmF : nullptr, lv.r,
                                 partial, st);

@@ -120,9 +120,12 @@ void launch_gs_phase(const LevDev& L, const double* coef, double* lam, const dou
 void launch_line_phase(const LevDev& L, const double* coef, double* lam, const double* f,
                        double* cpb, double* dpb, int c, cudaStream_t st);
 void launch_sum_ordered(const double* v, int n, double* out, cudaStream_t st);
-// y = K x (f == NULL) or y = f - K x; optional block partials of sum y^2
+// y = K x (f == NULL) or y = f - K x; optional block partials of sum y^2;
+// variant < 0: the process default (env WD_APPLY_VARIANT); 4: one plane per
+// CTA layer (small levels)
 int launch_apply(const LevDev& L, const double* coef, const double* x, const double* f,
-                 double* y, double* partial, cudaStream_t st);
+                 double* y, double* partial, cudaStream_t st, int variant = -1);
+constexpr long long APPLY_SMALL_COLS = 100LL * 100LL;   // measured crossover ~100^2 (189^2: 14.5 -> 20.1 us)
 void launch_reduce_sum(const double* partial, int n, double* out, cudaStream_t st);
 void launch_norm2_partial(const LevDev& L, const double* v, double* partial, int* nblk,
                           cudaStream_t st);
