@@ -517,6 +517,8 @@ int gs_fused2_prepare() {
                          (int)Geo<TJ_SWEEP>::SMEM);
     cudaFuncSetAttribute(gs_fused2_kernel<1, TJ_RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Geo<TJ_RES>::SMEM_RES);
+    cudaFuncSetAttribute(gs_fused2_kernel<0, TJ_RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Geo<TJ_RES>::SMEM);
     cudaFuncSetAttribute(gs_fused2_kernel<2, TJ_SWEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Geo<TJ_SWEEP>::SMEM_PRO);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -548,7 +550,12 @@ int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
         // backward neighbour p - d_s: row j - dy, plane z - dz (x shift per thread)
         KB.kb[s] = coef + (i64)s * L.NT - (i64)dy * L.sj - (i64)dz * L.sk;
     }
-    const int tj = partial ? TJ_RES : TJ_SWEEP;
+    // small levels (n1 < 200): the plain sweep on 64 x 6 tiles too (more, shorter
+    // tiles for the few CTAs such a level keeps busy: Paper-scale 189^2 / 95^2 / 48^2
+    // sweeps 31 / 26 / 18 -> 26 / 22 / 15 us; from 376^2 up the 64 x 8 tiles are
+    // faster).  Any tiling gives the same node updates (bitwise)
+    const bool small6 = !partial && !pro && tr1 < 0 && L.n1 < 200;
+    const int tj = (partial || small6) ? TJ_RES : TJ_SWEEP;
     int jt0 = L.own0 - ((L.own0 + L.jg0) & 1);
     const int ntx = (L.n1 + TI - 1) / TI;
     int nty = (L.own1 - jt0 + tj - 1) / tj;
@@ -572,7 +579,12 @@ int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
         PA.coy = pro->M.co[1];
         PA.w = pro->w;
     }
-    if (partial) {
+    if (small6) {
+        using G = Geo<TJ_RES>;
+        gs_fused2_kernel<0, TJ_RES><<<grid, G::THREADS, G::SMEM, st>>>(
+            *(const CUtensorMap*)ring_map_res, KB, L, lout, f, jt0, ntx, ntx * nty, g_test_jitter,
+            nullptr, PA);
+    } else if (partial) {
         using G = Geo<TJ_RES>;
         gs_fused2_kernel<1, TJ_RES><<<grid, G::THREADS, G::SMEM_RES, st>>>(
             *(const CUtensorMap*)ring_map_res, KB, L, lout, f, jt0, ntx, ntx * nty, g_test_jitter,
