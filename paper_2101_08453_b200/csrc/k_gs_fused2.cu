@@ -26,7 +26,8 @@
 //     is one 32-bit node offset (+ the thread's x shift) scaled onto a base
 //     instead of a 64-bit multiply-add chain per load;
 //   * ring addressing: plane slots advance incrementally (no modulo per step).
-// The residual variant runs 64 x 6 tiles (Geo<TJ_RES>; see TJ_SWEEP below).
+// The residual variant runs 64 x 6 tiles, the plain sweep on small levels 64 x 4
+// (Geo<TJ_RES>, Geo<TJ_SMALL>; see TJ_SWEEP below).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -82,7 +83,7 @@ struct Geo {
 // variant 64 x 6 tiles (14 colour warps, 16 in all): its 8-plane shadow makes
 // it register- and L1-tighter, and at Paper-scale level 0 it measured 5.34 ms
 // on 64 x 6 against 6.08 ms on 64 x 8 (the plain sweep: 4.67 against 4.54)
-constexpr int TJ_SWEEP = 8, TJ_RES = 6;
+constexpr int TJ_SWEEP = 8, TJ_RES = 6, TJ_SMALL = 4;
 
 namespace {
 
@@ -488,13 +489,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
 // ring box of one plane: 36 positions x 2 halves x 1 plane x 11 rows; the
 // position extent is the grid's (ceil(n1/2)), so the padding of a half row
 // and everything outside the grid read as zeros
-int make_ring_map(const LevDev& L, const double* v, void* map, bool res) {
+int make_ring_map(const LevDev& L, const double* v, void* map, int tj) {
     auto enc = encode_fn2();
     if (!enc) return -1;
     cuuint64_t dims[4] = {(cuuint64_t)((L.n1 + 1) / 2), 2, (cuuint64_t)L.n3, (cuuint64_t)L.n2};
     cuuint64_t str[3] = {(cuuint64_t)L.H * 8, (cuuint64_t)L.sk * 8, (cuuint64_t)L.sj * 8};
     cuuint32_t es[4] = {1, 1, 1, 1};
-    cuuint32_t box[4] = {SW, 2, 1, (cuuint32_t)(res ? Geo<TJ_RES>::SH : Geo<TJ_SWEEP>::SH)};
+    cuuint32_t box[4] = {SW, 2, 1, (cuuint32_t)(tj + 3)};   // Geo<tj>::SH
     static const CUtensorMapL2promotion promo[4] = {
         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
@@ -517,8 +518,8 @@ int gs_fused2_prepare() {
                          (int)Geo<TJ_SWEEP>::SMEM);
     cudaFuncSetAttribute(gs_fused2_kernel<1, TJ_RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Geo<TJ_RES>::SMEM_RES);
-    cudaFuncSetAttribute(gs_fused2_kernel<0, TJ_RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Geo<TJ_RES>::SMEM);
+    cudaFuncSetAttribute(gs_fused2_kernel<0, TJ_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Geo<TJ_SMALL>::SMEM);
     cudaFuncSetAttribute(gs_fused2_kernel<2, TJ_SWEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Geo<TJ_SWEEP>::SMEM_PRO);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -540,8 +541,9 @@ void gs_fused2_tile_rows(const LevDev& L, int w, int* b0, int* b1, int* nty) {
 }
 
 int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
-                     const void* ring_map_res, double* lout, const double* f, cudaStream_t st,
-                     double* partial, const ProlongIn* pro, int tr0, int tr1) {
+                     const void* ring_map_res, const void* ring_map_small, double* lout,
+                     const double* f, cudaStream_t st, double* partial, const ProlongIn* pro,
+                     int tr0, int tr1) {
     const int nsm = gs_fused2_prepare();
     KBase KB;
     for (int s = 0; s < 14; s++) {
@@ -550,12 +552,13 @@ int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
         // backward neighbour p - d_s: row j - dy, plane z - dz (x shift per thread)
         KB.kb[s] = coef + (i64)s * L.NT - (i64)dy * L.sj - (i64)dz * L.sk;
     }
-    // small levels (n1 < 200): the plain sweep on 64 x 6 tiles too (more, shorter
-    // tiles for the few CTAs such a level keeps busy: Paper-scale 189^2 / 95^2 / 48^2
-    // sweeps 31 / 26 / 18 -> 26 / 22 / 15 us; from 376^2 up the 64 x 8 tiles are
-    // faster).  Any tiling gives the same node updates (bitwise)
-    const bool small6 = !partial && !pro && tr1 < 0 && L.n1 < 200;
-    const int tj = (partial || small6) ? TJ_RES : TJ_SWEEP;
+    // small levels (n1 < 200): the plain sweep on 64 x 4 tiles (more, shorter
+    // tiles for the few CTAs such a level keeps busy: Small's V-cycle -17 %,
+    // Paper-scale 189^2 / 95^2 / 48^2 sweeps 31 / 26 / 18 -> 26 / 22 / 15 us on
+    // 64 x 6 and less on 64 x 4; from 251^2 up the 64 x 8 tiles are faster).
+    // Any tiling gives the same node updates (bitwise)
+    const bool small = !partial && !pro && tr1 < 0 && L.n1 < 200;
+    const int tj = partial ? TJ_RES : small ? TJ_SMALL : TJ_SWEEP;
     int jt0 = L.own0 - ((L.own0 + L.jg0) & 1);
     const int ntx = (L.n1 + TI - 1) / TI;
     int nty = (L.own1 - jt0 + tj - 1) / tj;
@@ -579,10 +582,10 @@ int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
         PA.coy = pro->M.co[1];
         PA.w = pro->w;
     }
-    if (small6) {
-        using G = Geo<TJ_RES>;
-        gs_fused2_kernel<0, TJ_RES><<<grid, G::THREADS, G::SMEM, st>>>(
-            *(const CUtensorMap*)ring_map_res, KB, L, lout, f, jt0, ntx, ntx * nty, g_test_jitter,
+    if (small) {
+        using G = Geo<TJ_SMALL>;
+        gs_fused2_kernel<0, TJ_SMALL><<<grid, G::THREADS, G::SMEM, st>>>(
+            *(const CUtensorMap*)ring_map_small, KB, L, lout, f, jt0, ntx, ntx * nty, g_test_jitter,
             nullptr, PA);
     } else if (partial) {
         using G = Geo<TJ_RES>;

@@ -158,6 +158,7 @@ struct Level {
     alignas(64) unsigned char tmA[128], tmB[128], tmX[128], tmF[128];
     alignas(64) unsigned char tmR[2][128];   // ring maps of raw[1] and raw[4] (k_gs_fused2.cu)
     alignas(64) unsigned char tmRr[2][128];  // the same for the residual variant's tiles
+    alignas(64) unsigned char tmRs[2][128];  // and for the small levels' plain tiles
 };
 
 struct Part {
@@ -681,10 +682,12 @@ int alloc_level(wd_ctx* ctx, Level& lv, bool galerkin) {
     launch_zero_unwritten(lv.L, lv.coef, galerkin, 0);
     CK(cudaStreamSynchronize(0));
     if (make_coef_maps(lv.L, lv.coef, lv.tmA, lv.tmB) || make_vec_map(lv.L, lv.lam, lv.tmX, true) ||
-        make_vec_map(lv.L, lv.f, lv.tmF, false) || make_ring_map(lv.L, lv.raw[1], lv.tmR[0], false) ||
-        make_ring_map(lv.L, lv.raw[4], lv.tmR[1], false) ||
-        make_ring_map(lv.L, lv.raw[1], lv.tmRr[0], true) ||
-        make_ring_map(lv.L, lv.raw[4], lv.tmRr[1], true))
+        make_vec_map(lv.L, lv.f, lv.tmF, false) || make_ring_map(lv.L, lv.raw[1], lv.tmR[0], 8) ||
+        make_ring_map(lv.L, lv.raw[4], lv.tmR[1], 8) ||
+        make_ring_map(lv.L, lv.raw[1], lv.tmRr[0], 6) ||
+        make_ring_map(lv.L, lv.raw[4], lv.tmRr[1], 6) ||
+        make_ring_map(lv.L, lv.raw[1], lv.tmRs[0], 4) ||
+        make_ring_map(lv.L, lv.raw[4], lv.tmRs[1], 4))
         return fail(WD_E_CUDA, "cuTensorMapEncodeTiled failed for level dims (%d,%d,%d)", lv.L.n1,
                     lv.L.n2, lv.L.n3);
     return WD_OK;
@@ -700,8 +703,8 @@ int gs_sweep_level(Level& F, cudaStream_t st, double* partial = nullptr,
     if (v2_level(F))
     {
         const int b = F.lam == F.raw[1] ? 0 : 1;
-        return launch_gs_fused2(F.L, F.coef, F.tmR[b], F.tmRr[b], F.lam2, F.f, st, partial, pro,
-                                tr0, tr1);
+        return launch_gs_fused2(F.L, F.coef, F.tmR[b], F.tmRr[b], F.tmRs[b], F.lam2, F.f, st,
+                                partial, pro, tr0, tr1);
     }
     return launch_gs_fused(F.L, F.coef, F.lam, F.lam2, F.f, st, partial);
 }

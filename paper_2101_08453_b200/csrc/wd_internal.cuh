@@ -163,7 +163,7 @@ int gs_fused_prepare();
 // k_gs_fused2.cu: the same sweep (bitwise) with a TMA-filled lambda ring and
 // 32-bit coupling offsets (needs NT < 2^31)
 extern int g_gs_v2;   // env WD_GS_V2=0: use k_gs_fused.cu
-int make_ring_map(const LevDev& L, const double* v, void* map, bool res);
+int make_ring_map(const LevDev& L, const double* v, void* map, int tj);   // box rows tj + 3
 int gs_fused2_prepare();
 // the prolongation folded into a sweep: lin + w P xc is the sweep's input
 // (identity-z transitions with horizontal coarsening only; k_gs_fused2.cu)
@@ -173,13 +173,14 @@ struct ProlongIn {
     MapDev M;
     double w;
 };
-// ring_map / ring_map_res: make_ring_map(.., res = false / true) of lin (the
-// plain / PRO sweeps tile 64 x 8, the residual variant (partial) 64 x 6)
-// tr0, tr1: only the tile rows [tr0, tr1) (plain / PRO sweeps; tr1 < 0: all)
+// ring_map / ring_map_res / ring_map_small: make_ring_map(.., tj = 8 / 6 / 4) of
+// lin (the plain / PRO sweeps tile 64 x 8, the residual variant (partial) 64 x 6,
+// the plain sweep on small levels 64 x 4); tr0, tr1: only the tile rows
+// [tr0, tr1) (plain / PRO sweeps on 64 x 8 tiles; tr1 < 0: all)
 int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
-                     const void* ring_map_res, double* lout, const double* f, cudaStream_t st,
-                     double* partial = nullptr, const ProlongIn* pro = nullptr, int tr0 = 0,
-                     int tr1 = -1);
+                     const void* ring_map_res, const void* ring_map_small, double* lout,
+                     const double* f, cudaStream_t st, double* partial = nullptr,
+                     const ProlongIn* pro = nullptr, int tr0 = 0, int tr1 = -1);
 void gs_fused2_tile_rows(const LevDev& L, int w, int* b0, int* b1, int* nty);
 
 // k_io.cu: steps either side of the path
