@@ -520,6 +520,8 @@ int gs_fused2_prepare() {
                          (int)Geo<TJ_RES>::SMEM_RES);
     cudaFuncSetAttribute(gs_fused2_kernel<0, TJ_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Geo<TJ_SMALL>::SMEM);
+    cudaFuncSetAttribute(gs_fused2_kernel<1, TJ_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Geo<TJ_SMALL>::SMEM_RES);
     cudaFuncSetAttribute(gs_fused2_kernel<2, TJ_SWEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Geo<TJ_SWEEP>::SMEM_PRO);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -557,8 +559,8 @@ int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
     // Paper-scale 189^2 / 95^2 / 48^2 sweeps 31 / 26 / 18 -> 26 / 22 / 15 us on
     // 64 x 6 and less on 64 x 4; from 251^2 up the 64 x 8 tiles are faster).
     // Any tiling gives the same node updates (bitwise)
-    const bool small = !partial && !pro && tr1 < 0 && L.n1 < 200;
-    const int tj = partial ? TJ_RES : small ? TJ_SMALL : TJ_SWEEP;
+    const bool small = !pro && tr1 < 0 && L.n1 < 200;
+    const int tj = small ? TJ_SMALL : partial ? TJ_RES : TJ_SWEEP;
     int jt0 = L.own0 - ((L.own0 + L.jg0) & 1);
     const int ntx = (L.n1 + TI - 1) / TI;
     int nty = (L.own1 - jt0 + tj - 1) / tj;
@@ -582,7 +584,12 @@ int launch_gs_fused2(const LevDev& L, const double* coef, const void* ring_map,
         PA.coy = pro->M.co[1];
         PA.w = pro->w;
     }
-    if (small) {
+    if (small && partial) {
+        using G = Geo<TJ_SMALL>;
+        gs_fused2_kernel<1, TJ_SMALL><<<grid, G::THREADS, G::SMEM_RES, st>>>(
+            *(const CUtensorMap*)ring_map_small, KB, L, lout, f, jt0, ntx, ntx * nty, g_test_jitter,
+            partial, PA);
+    } else if (small) {
         using G = Geo<TJ_SMALL>;
         gs_fused2_kernel<0, TJ_SMALL><<<grid, G::THREADS, G::SMEM, st>>>(
             *(const CUtensorMap*)ring_map_small, KB, L, lout, f, jt0, ntx, ntx * nty, g_test_jitter,
