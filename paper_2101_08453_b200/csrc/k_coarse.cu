@@ -4,7 +4,7 @@
 // Setup: the free block of the coarsest stencil is expanded into a dense SPD
 // matrix (natural order of free nodes) and inverted in place on the device by
 // blocked Gauss-Jordan elimination without pivoting (SPD), 32x32 blocks,
-// four launches per block step.  Per V-cycle: one GEMV with the explicit
+// three launches per block step.  Per V-cycle: one GEMV with the explicit
 // inverse (<= 4096^2 doubles, L2 resident), fused with the gather of the
 // free right-hand side and the scatter of the solution.
 #include "wd_internal.cuh"
@@ -44,41 +44,41 @@ __global__ void dense_build_kernel(LevDev L, const double* __restrict__ K, doubl
             }
 }
 
-// (1) invert the diagonal block in shared memory (scalar Gauss-Jordan,
-//     double-buffered: one barrier per pivot, one division per pivot)
-__global__ void gj_diag_kernel(const double* __restrict__ A, int n, int k0, int nb, double* Dinv) {
-    __shared__ double D[2][BS][BS + 1];
+// (1) + (2) diagonal block inversion in shared memory (scalar Gauss-Jordan,
+//     double-buffered: one barrier per pivot, one division per pivot) fused
+//     with the row panel:
+// (2) row panel: A_Kj <- Dinv A_Kj  (j outside block K).  Every CTA inverts
+//     the diagonal block itself (the same operations as gj_diag_kernel, so the
+//     same Dinv bit for bit) instead of waiting for a separate launch; the CTA
+//     of block K writes Dinv for the column panel
+__global__ void gj_rowdiag_kernel(double* A, int n, int k0, int nb, double* Dinv) {
+    const int kb = k0 / BS;
+    __shared__ double D2[2][BS][BS + 1], S[BS][BS + 1];
     const int r = threadIdx.y, c = threadIdx.x;
-    D[0][r][c] = (r < nb && c < nb) ? A[(i64)(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
+    D2[0][r][c] = (r < nb && c < nb) ? A[(i64)(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
+    const int j = blockIdx.x * BS + c;
+    if ((int)blockIdx.x != kb) S[r][c] = (r < nb && j < n) ? A[(i64)(k0 + r) * n + j] : 0.0;
     __syncthreads();
     int b = 0;
     for (int t = 0; t < BS; t++) {
-        const double (&S)[BS][BS + 1] = D[b];
-        const double piv = S[t][t];
-        const double ip = 1.0 / piv;   // every thread, same value (no extra barrier)
-        const double drt = S[r][t], dtc = S[t][c], drc = S[r][c];
+        const double (&Q)[BS][BS + 1] = D2[b];
+        const double piv = Q[t][t];
+        const double ip = 1.0 / piv;
+        const double drt = Q[r][t], dtc = Q[t][c], drc = Q[r][c];
         double v;
         if (r == t && c == t) v = ip;
         else if (r == t) v = dtc * ip;
         else if (c == t) v = -drt * ip;
         else v = drc - drt * (dtc * ip);
-        D[b ^ 1][r][c] = v;
+        D2[b ^ 1][r][c] = v;
         b ^= 1;
         __syncthreads();
     }
-    Dinv[r * BS + c] = D[b][r][c];
-}
-
-// (2) row panel: A_Kj <- Dinv A_Kj  (j outside block K)
-__global__ void gj_row_kernel(double* A, int n, int k0, int nb, const double* __restrict__ Dinv) {
-    const int kb = k0 / BS;
-    if ((int)blockIdx.x == kb) return;
-    __shared__ double D[BS][BS + 1], S[BS][BS + 1];
-    const int r = threadIdx.y, c = threadIdx.x;
-    const int j = blockIdx.x * BS + c;
-    D[r][c] = Dinv[r * BS + c];
-    S[r][c] = (r < nb && j < n) ? A[(i64)(k0 + r) * n + j] : 0.0;
-    __syncthreads();
+    const double (&D)[BS][BS + 1] = D2[b];
+    if ((int)blockIdx.x == kb) {
+        Dinv[r * BS + c] = D[r][c];
+        return;
+    }
     if (r < nb && j < n) {
         double s = 0.0;
         for (int t = 0; t < nb; t++) s = fma(D[r][t], S[t][c], s);
@@ -202,9 +202,8 @@ int gj_invert(double* A, int n, double* Dinv, cudaStream_t st) {
     dim3 blk(BS, BS);
     for (int kb = 0; kb < nbk; kb++) {
         const int k0 = kb * BS, nb = (n - k0) < BS ? (n - k0) : BS;
-        g_launches += 4;
-        gj_diag_kernel<<<1, blk, 0, st>>>(A, n, k0, nb, Dinv);
-        gj_row_kernel<<<nbk, blk, 0, st>>>(A, n, k0, nb, Dinv);
+        g_launches += 3;
+        gj_rowdiag_kernel<<<nbk, blk, 0, st>>>(A, n, k0, nb, Dinv);
         const int ntt = (n + TT - 1) / TT;
         gj_trail_kernel<<<dim3(ntt, ntt), 256, 0, st>>>(A, n, k0, nb);
         gj_col_kernel<<<nbk, blk, 0, st>>>(A, n, k0, nb, Dinv);
