@@ -44,13 +44,12 @@ __global__ void dense_build_kernel(LevDev L, const double* __restrict__ K, doubl
             }
 }
 
-// (1) + (2) diagonal block inversion in shared memory (scalar Gauss-Jordan,
-//     double-buffered: one barrier per pivot, one division per pivot) fused
-//     with the row panel:
-// (2) row panel: A_Kj <- Dinv A_Kj  (j outside block K).  Every CTA inverts
-//     the diagonal block itself (the same operations as gj_diag_kernel, so the
-//     same Dinv bit for bit) instead of waiting for a separate launch; the CTA
-//     of block K writes Dinv for the column panel
+// (1) + (2) the diagonal block's inverse Dinv (scalar Gauss-Jordan in shared
+//     memory, double-buffered: one barrier and one division per pivot) fused
+//     with the row panel A_Kj <- Dinv A_Kj (j outside block K): every CTA
+//     inverts the diagonal block itself (identical operations, so identical
+//     Dinv) instead of waiting for a separate launch, and the CTA of block K
+//     writes Dinv for the column panel
 __global__ void gj_rowdiag_kernel(double* A, int n, int k0, int nb, double* Dinv) {
     const int kb = k0 / BS;
     __shared__ double D2[2][BS][BS + 1], S[BS][BS + 1];
