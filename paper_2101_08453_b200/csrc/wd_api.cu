@@ -294,6 +294,15 @@ struct wd_ctx {
     long long graph_kernels = 0;
     cudaEvent_t ev_gs[32] = {};
     cudaEvent_t ev_cyc[2] = {};
+    // wd_solve's split cycles: the start of cycle c on ev_cs[c & 1] (so that
+    // its events can be read one cycle later, while the GPU already runs the
+    // next one -- waiting for them at once would idle the GPU every cycle)
+    cudaEvent_t ev_cs[2] = {};
+    int cyc_par = 0;
+    bool pend_rest = false;    // the last split cycle's rest not yet read
+    int pend_par = 0;
+    bool pend_first = false;   // the last split cycle's first sweep not yet read
+    bool pend_first_res = false;
     bool first_res = false;    // the last cycle's first sweep was the residual variant
     cudaEvent_t ev_res[2] = {};
     cudaEvent_t ev_ap[2] = {};   // the level-0 residual before the restriction
@@ -1127,6 +1136,48 @@ void profile_accumulate(wd_ctx* ctx, bool cycle, bool resid) {
     cudaGetLastError();
 }
 
+// wd_solve's split cycles (profile mode): the first level-0 sweep of a cycle
+// (events ev_gs[0..1]) and the rest of it (the other level-0 sweeps, the
+// residual before the restriction, the cycle) are read separately, each just
+// before the events are recorded again -- after the GPU has been given the
+// next work, so the reads never leave it idle
+void profile_first(wd_ctx* ctx) {
+    if (!ctx->opt.profile || !ctx->pend_first) return;
+    ctx->pend_first = false;
+    float ms;
+    if (ctx->nlev > 1 && ctx->parts.size() == 1 && cudaEventSynchronize(ctx->ev_gs[1]) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, ctx->ev_gs[0], ctx->ev_gs[1]) == cudaSuccess) {
+        const int slot = ctx->pend_first_res ? 6 : 0;
+        ctx->prof[slot] += ms;
+        ctx->prof[slot + 1] += 1;
+    }
+    cudaGetLastError();
+}
+
+void profile_rest(wd_ctx* ctx) {
+    if (!ctx->opt.profile || !ctx->pend_rest) return;
+    ctx->pend_rest = false;
+    cudaEventSynchronize(ctx->ev_cyc[1]);
+    float ms;
+    const int ns = std::min(ctx->opt.pre_smooth + ctx->opt.post_smooth, 16);
+    if (ctx->nlev > 1 && ctx->parts.size() == 1) {
+        for (int sw = 1; sw < ns; sw++)
+            if (cudaEventElapsedTime(&ms, ctx->ev_gs[2 * sw], ctx->ev_gs[2 * sw + 1]) == cudaSuccess) {
+                ctx->prof[0] += ms;
+                ctx->prof[1] += 1;
+            }
+        if (cudaEventElapsedTime(&ms, ctx->ev_ap[0], ctx->ev_ap[1]) == cudaSuccess) {
+            ctx->prof[8] += ms;
+            ctx->prof[9] += 1;
+        }
+    }
+    if (cudaEventElapsedTime(&ms, ctx->ev_cs[ctx->pend_par], ctx->ev_cyc[1]) == cudaSuccess) {
+        ctx->prof[2] += ms;
+        ctx->prof[3] += 1;
+    }
+    cudaGetLastError();
+}
+
 int run_vcycle(wd_ctx* ctx, cudaStream_t st) {
     ctx->first_res = false;
     if (ctx->opt.profile) CK(cudaEventRecord(ctx->ev_cyc[0], st));
@@ -1178,7 +1229,7 @@ int capture_graph(wd_ctx* ctx, cudaGraphExec_t* out, long long* nk, Fn fn) {
 // the rest of the cycle ends with the iterate back in the canonical buffer).
 int run_split(wd_ctx* ctx, int which, cudaStream_t st) {
     const bool prof = ctx->opt.profile && ctx->parts.size() == 1;
-    if (which < 2 && ctx->opt.profile) CK(cudaEventRecord(ctx->ev_cyc[0], st));
+    if (which < 2 && ctx->opt.profile) CK(cudaEventRecord(ctx->ev_cs[ctx->cyc_par], st));
     auto body = [&](cudaStream_t s) -> int {
         if (which == 0) return smooth_first_res(ctx, prof, s);
         if (which == 1) return smooth(ctx, 0, prof, 0, s);
@@ -1555,6 +1606,7 @@ void wd_destroy(wd_ctx* ctx) {
     for (auto e : ctx->pev) if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_gs) if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_cyc) if (e) cudaEventDestroy(e);
+    for (auto e : ctx->ev_cs) if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_res) if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_ap) if (e) cudaEventDestroy(e);
     for (Part& P : ctx->parts) {
@@ -1759,6 +1811,7 @@ static int assemble_impl(const double* X, const double* Y, const double* Z, int 
     if (o.profile) {
         for (auto& e : ctx->ev_gs) CK(cudaEventCreate(&e));
         for (auto& e : ctx->ev_cyc) CK(cudaEventCreate(&e));
+        for (auto& e : ctx->ev_cs) CK(cudaEventCreate(&e));
         for (auto& e : ctx->ev_res) CK(cudaEventCreate(&e));
         for (auto& e : ctx->ev_ap) CK(cudaEventCreate(&e));
     }
@@ -2351,6 +2404,7 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
     RoleGuard roles(ctx);
     if (!(rel_tol > 0.0 && rel_tol < 1.0)) return fail(WD_E_INVAL, "rel_tol must be in (0,1)");
     cudaStream_t st = (cudaStream_t)stream;
+    ctx->pend_first = ctx->pend_rest = false;
     Stage sf, s0, sl;
     RC(stage_in(ctx, sf, f, abi_nodes(ctx), st));
     if (lambda0) RC(stage_in(ctx, s0, lambda0, abi_nodes(ctx), st));
@@ -2444,8 +2498,13 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
             Nvtx n_cyc("cycle %d", c + 1);
             bool first_done = false;
             if (!have) {   // first sweep of cycle c+1, returning the residual of lam_c
+                profile_first(ctx);    // the previous cycle's, before its events are reused
+                ctx->cyc_par ^= 1;
                 RC(run_split(ctx, 0, st));
                 RC(fetch_scalars(ctx, 1, st));
+                profile_rest(ctx);     // the previous cycle has finished
+                ctx->pend_first = true;
+                ctx->pend_first_res = true;
                 first_done = true;
             }
             const double rel = std::sqrt(ctx->hscal[0]) / fn;
@@ -2472,22 +2531,37 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
                 profile_accumulate(ctx, true, true);
                 continue;
             }
-            if (!first_done) RC(run_split(ctx, 1, st));
+            if (!first_done) {
+                profile_first(ctx);
+                ctx->cyc_par ^= 1;
+                RC(run_split(ctx, 1, st));
+                ctx->pend_first = true;
+                ctx->pend_first_res = false;
+            }
             ctx->first_res = first_done;
+            profile_rest(ctx);   // (already read: a no-op)
             RC(run_split(ctx, 2, st));
+            ctx->pend_rest = ctx->opt.profile;
+            ctx->pend_par = ctx->cyc_par;
             c++;
-            profile_accumulate(ctx, true, false);
             const double prev = c >= 2 ? ring4[(c - 2) & 3] : 0.0;
             const bool predicted = prev > 0.0 && rel * (rel / prev) <= rel_tol;
             if (predicted || c >= ctx->opt.max_cycles) {
                 RC(residual_sq(ctx, 0, st));
                 RC(fetch_scalars(ctx, 1, st));
+                profile_first(ctx);
+                profile_rest(ctx);
                 profile_accumulate(ctx, false, true);
                 have = true;
             } else {
                 have = false;
             }
         }
+    }
+    if (ctx->opt.profile && (ctx->pend_first || ctx->pend_rest)) {
+        CK(cudaStreamSynchronize(st));
+        profile_first(ctx);
+        profile_rest(ctx);
     }
     R.cycles = c;
     R.status = status;
