@@ -329,6 +329,7 @@ def run_ours(args, ws, rank, local):
     cycles, gs_ms, gs_sweeps, vc_ms, vc_n, rates = 0, 0.0, 0, 0.0, 0, []
     gsr_ms, gsr_sweeps = 0.0, 0
     ap_ms, ap_n, rs_ms, rs_n = 0.0, 0, 0.0, 0
+    n_plain_all, n_res_all = 0, 0   # level-0 sweeps executed (timed ones are a sample)
     with Clocks(local) as clk:
         start.record(stream)
         for _ in range(args.steps):
@@ -347,6 +348,8 @@ def run_ours(args, ws, rank, local):
             rs_n += int(prof["resids"])
             vc_ms += prof["vcycle_ms"]
             vc_n += int(prof["vcycles"])
+            n_plain_all += int(prof["gs0_sweeps_all"])
+            n_res_all += int(prof["gs0res_sweeps_all"])
             info = hier_info(ctx)
             ctx.close()   # frees device memory; ordered after the step's work
         stop.record(stream)
@@ -368,14 +371,17 @@ def run_ours(args, ws, rank, local):
         free0 = (n1 - 2) * (n2 - 2) * (n3 - 1)
     gs_kind = args.smoother
     gs_b, gs_per_sweep, gs_name = GS_BYTES[gs_kind]
-    # every level-0 sweep of the timed steps, the residual variant included
-    # (time-weighted: algorithmic bytes of all launches over their total time)
-    n_all = gs_sweeps + gsr_sweeps
-    launch_ms = (gs_ms + gsr_ms) / max(n_all, 1) / gs_per_sweep
-    bytes_launch = gs_b * free0
-    achieved = bytes_launch / (launch_ms * 1e-3) / 1e9 if launch_ms > 0 else 0.0
+    # every level-0 sweep of the timed steps, the residual variant included,
+    # time-weighted: the mean launch time of each variant (from the timed
+    # sample: the sweeps of every 4th V-cycle) weighted by how many of each ran
     plain_ms = gs_ms / max(gs_sweeps, 1) / gs_per_sweep
     res_ms = gsr_ms / max(gsr_sweeps, 1) if gsr_sweeps else None
+    if n_plain_all + n_res_all == 0:   # no split cycles (phased smoother): all timed
+        n_plain_all, n_res_all = gs_sweeps, gsr_sweeps
+    n_all = n_plain_all + n_res_all
+    launch_ms = (n_plain_all * plain_ms * gs_per_sweep + n_res_all * (res_ms or 0.0)) / max(n_all, 1) / gs_per_sweep
+    bytes_launch = gs_b * free0
+    achieved = bytes_launch / (launch_ms * 1e-3) / 1e9 if launch_ms > 0 else 0.0
     traffic, traffic_res = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_gs_traffic.json")
     if os.path.exists(tp):
@@ -387,7 +393,7 @@ def run_ours(args, ws, rank, local):
             traffic = None
     if traffic is not None and traffic_res is not None and n_all:
         # per launch, weighted like `achieved` (plain and residual-variant launches)
-        traffic_all = (traffic * gs_sweeps + traffic_res * gsr_sweeps) / n_all
+        traffic_all = (traffic * n_plain_all + traffic_res * n_res_all) / n_all
     else:
         traffic_all = traffic
 
@@ -395,13 +401,16 @@ def run_ours(args, ws, rank, local):
     # level-0 operator pass of the timed steps (the residual before the
     # restriction, 136 B/node; the residual-norm passes, 128 B/node: no r
     # written), algorithmic bytes over their summed device time
-    op_bytes = gs_b * free0 * n_all * gs_per_sweep + 136 * free0 * ap_n + 128 * free0 * rs_n
-    op_ms = gs_ms + gsr_ms + ap_ms + rs_ms
+    # (sampled sweeps and residuals before the restriction scaled to every launch)
+    ap_all = vc_n if ap_n else 0
+    ap_mean = ap_ms / ap_n if ap_n else 0.0
+    op_bytes = gs_b * free0 * n_all * gs_per_sweep + 136 * free0 * ap_all + 128 * free0 * rs_n
+    op_ms = launch_ms * gs_per_sweep * n_all + ap_mean * ap_all + rs_ms
     op_gbs = op_bytes / (op_ms * 1e-3) / 1e9 if op_ms > 0 else 0.0
     op_obj = {"kernels": f"{gs_name} (plain + residual variant) + apply_tma_kernel (residual "
                          "before the restriction; residual-norm passes), level 0",
               "achieved": op_gbs, "frac": op_gbs / peak, "ms": op_ms,
-              "launches": n_all * gs_per_sweep + ap_n + rs_n}
+              "launches": n_all * gs_per_sweep + ap_all + rs_n}
 
     line = None
     if rank == 0:
@@ -428,15 +437,21 @@ def run_ours(args, ws, rank, local):
             "device_bytes": dev_bytes,
             "roofline": {"kernel": f"{gs_name} (level 0, all sweeps incl. the residual "
                                    "variant, time-weighted)", "bound": "hbm",
+                         "sampling": "CUDA events around every level-0 sweep of every 4th "
+                                     "V-cycle of the timed steps (event nodes in the graphs "
+                                     "cost ~6 us each)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_all,
                          "bytes_per_launch": bytes_launch, "launch_ms": launch_ms,
                          "launches": n_all * gs_per_sweep,
-                         "plain": {"launch_ms": plain_ms, "launches": gs_sweeps * gs_per_sweep,
+                         "launches_timed": (gs_sweeps + gsr_sweeps) * gs_per_sweep,
+                         "plain": {"launch_ms": plain_ms, "launches": n_plain_all * gs_per_sweep,
+                                   "launches_timed": gs_sweeps * gs_per_sweep,
                                    "traffic": traffic,
                                    "frac": (bytes_launch / (plain_ms * 1e-3) / 1e9 / peak
                                             if plain_ms > 0 else None)},
-                         "residual_variant": {"launch_ms": res_ms, "launches": gsr_sweeps,
+                         "residual_variant": {"launch_ms": res_ms, "launches": n_res_all,
+                                              "launches_timed": gsr_sweeps,
                                               "traffic": traffic_res,
                                               "frac": (bytes_launch / (res_ms * 1e-3) / 1e9 / peak
                                                        if res_ms else None)},

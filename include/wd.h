@@ -259,8 +259,11 @@ int wd_residual_norm(wd_ctx* ctx, const double* x, const double* f, double* abs_
  *          (the first sweep of a cycle in wd_solve)   out[7] their number
  *   out[8] ms in the level-0 residual r = f - K lambda before the restriction
  *          (one per V-cycle)                 out[9] their number
+ *   out[10], out[11]: plain / residual-returning level-0 sweeps executed in
+ *          wd_solve's split cycles, timed or not (wd_solve times the sweeps
+ *          of every 4th cycle only; these counts weight the sampled times)
  * A sweep is one launch of the fused smoother (four launches with
- * WD_SMOOTH_PHASED).  Returns the number of values written (<= n, <= 10). */
+ * WD_SMOOTH_PHASED).  Returns the number of values written (<= n, <= 12). */
 int wd_profile_read(const wd_ctx* ctx, double* out, int n);
 /* Reset the accumulated profile. */
 void wd_profile_reset(wd_ctx* ctx);

@@ -225,10 +225,11 @@ class Context:
 
 
 def wd_profile_read(ctx: Context):
-    out = (C.c_double * 10)()
-    _lib.wd_profile_read(ctx.h, out, 10)
+    out = (C.c_double * 12)()
+    _lib.wd_profile_read(ctx.h, out, 12)
     keys = ("gs0_ms", "gs0_sweeps", "vcycle_ms", "vcycles", "resid_ms", "resids", "gs0res_ms",
-            "gs0res_sweeps", "apply0_ms", "apply0_launches")
+            "gs0res_sweeps", "apply0_ms", "apply0_launches", "gs0_sweeps_all",
+            "gs0res_sweeps_all")
     return dict(zip(keys, list(out)))
 
 

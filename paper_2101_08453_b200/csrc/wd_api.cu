@@ -279,8 +279,13 @@ struct wd_ctx {
     // wd_solve with the fused smoother: the V-cycle split after its first
     // level-0 sweep; that sweep also returns the residual of its input
     // (k_gs_fused.cu RES), so the convergence test needs no residual pass
-    cudaGraphExec_t g_first_res = nullptr, g_first = nullptr, g_rest = nullptr;
-    long long k_first_res = 0, k_first = 0, k_rest = 0;
+    // [1]: the profiling variant, with event records around the level-0
+    // sweeps (used on every PROF_EVERY-th cycle when opt.profile is on; the
+    // event nodes cost ~6 us each, 23 % of a Small solve if on every cycle)
+    cudaGraphExec_t g_first_res[2] = {}, g_first[2] = {}, g_rest[2] = {};
+    long long k_first_res[2] = {}, k_first[2] = {}, k_rest[2] = {};
+    bool cyc_evented = false;   // the current split cycle uses the profiling variant
+    bool prof_on = true;        // vcycle_level may record its profiling events
     // the whole cycle loop as one graph (conditional WHILE node), its kernel
     // counts per body and the device / pinned host copies of its state
     cudaGraphExec_t g_loop = nullptr;
@@ -300,13 +305,14 @@ struct wd_ctx {
     cudaEvent_t ev_cs[2] = {};
     int cyc_par = 0;
     bool pend_rest = false;    // the last split cycle's rest not yet read
+    bool pend_rest_sweeps = false;   // ... including its sweep / residual events
     int pend_par = 0;
     bool pend_first = false;   // the last split cycle's first sweep not yet read
     bool pend_first_res = false;
     bool first_res = false;    // the last cycle's first sweep was the residual variant
     cudaEvent_t ev_res[2] = {};
     cudaEvent_t ev_ap[2] = {};   // the level-0 residual before the restriction
-    double prof[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    double prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     // weight w of the coarse-grid correction lam += w P lam_c: 1 (Eq. (7));
     // env WD_TEST_CORRECTION_WEIGHT sets another value, only so that the tests
     // can drive a cycle to divergence and exercise the WD_E_DIVERGED guard
@@ -1050,7 +1056,7 @@ int vcycle_level(wd_ctx* ctx, int l, cudaStream_t st, int first = 0) {
         Nvtx nc("coarsest solve");
         return coarse_solve(ctx, st);
     }
-    const bool prof = ctx->opt.profile && l == 0 && ctx->parts.size() == 1;
+    const bool prof = ctx->opt.profile && ctx->prof_on && l == 0 && ctx->parts.size() == 1;
     int ns = first;
     {
         Nvtx n_("pre-smoothing");
@@ -1136,6 +1142,10 @@ void profile_accumulate(wd_ctx* ctx, bool cycle, bool resid) {
     cudaGetLastError();
 }
 
+// profile mode: the level-0 sweeps of every PROF_EVERY-th split cycle are
+// timed (event records in the graphs); the cycle times of all cycles
+constexpr int PROF_EVERY = 4;
+
 // wd_solve's split cycles (profile mode): the first level-0 sweep of a cycle
 // (events ev_gs[0..1]) and the rest of it (the other level-0 sweeps, the
 // residual before the restriction, the cycle) are read separately, each just
@@ -1160,7 +1170,7 @@ void profile_rest(wd_ctx* ctx) {
     cudaEventSynchronize(ctx->ev_cyc[1]);
     float ms;
     const int ns = std::min(ctx->opt.pre_smooth + ctx->opt.post_smooth, 16);
-    if (ctx->nlev > 1 && ctx->parts.size() == 1) {
+    if (ctx->pend_rest_sweeps && ctx->nlev > 1 && ctx->parts.size() == 1) {
         for (int sw = 1; sw < ns; sw++)
             if (cudaEventElapsedTime(&ms, ctx->ev_gs[2 * sw], ctx->ev_gs[2 * sw + 1]) == cudaSuccess) {
                 ctx->prof[0] += ms;
@@ -1228,7 +1238,13 @@ int capture_graph(wd_ctx* ctx, cudaGraphExec_t* out, long long* nk, Fn fn) {
 // roles follow the stream order (the first sweep swaps lam/lam2 of level 0;
 // the rest of the cycle ends with the iterate back in the canonical buffer).
 int run_split(wd_ctx* ctx, int which, cudaStream_t st) {
-    const bool prof = ctx->opt.profile && ctx->parts.size() == 1;
+    const int set = ctx->opt.profile && ctx->cyc_evented ? 1 : 0;
+    const bool prof = set == 1 && ctx->parts.size() == 1;
+    struct ProfOn {   // vcycle_level records events only in the profiling variant
+        wd_ctx* c;
+        ProfOn(wd_ctx* x, bool on) : c(x) { c->prof_on = on; }
+        ~ProfOn() { c->prof_on = true; }
+    } prof_on_(ctx, set == 1);
     if (which < 2 && ctx->opt.profile) CK(cudaEventRecord(ctx->ev_cs[ctx->cyc_par], st));
     auto body = [&](cudaStream_t s) -> int {
         if (which == 0) return smooth_first_res(ctx, prof, s);
@@ -1238,7 +1254,7 @@ int run_split(wd_ctx* ctx, int which, cudaStream_t st) {
     if (!ctx->opt.use_graph) {
         RC(body(st));
     } else {
-        if (!ctx->g_first_res) {
+        if (!ctx->g_first_res[set]) {
             if (which == 2) return fail(WD_E_INVAL, "split V-cycle: rest before first sweep");
             // capture all three from the canonical state: the two first-sweep
             // variants each swap the level-0 buffers, the rest swaps them back
@@ -1258,13 +1274,15 @@ int run_split(wd_ctx* ctx, int which, cudaStream_t st) {
                     if (g) cudaGraphExecDestroy(g);
                 return rc;
             }
-            ctx->g_first = g1, ctx->g_first_res = g0, ctx->g_rest = g2;
-            ctx->k_first = k1, ctx->k_first_res = k0, ctx->k_rest = k2;
+            ctx->g_first[set] = g1, ctx->g_first_res[set] = g0, ctx->g_rest[set] = g2;
+            ctx->k_first[set] = k1, ctx->k_first_res[set] = k0, ctx->k_rest[set] = k2;
             // host roles now canonical; replay the first sweep's swap below
         }
-        cudaGraphExec_t g = which == 0 ? ctx->g_first_res : which == 1 ? ctx->g_first : ctx->g_rest;
+        cudaGraphExec_t g = which == 0 ? ctx->g_first_res[set] : which == 1 ? ctx->g_first[set]
+                                                               : ctx->g_rest[set];
         CK(cudaGraphLaunch(g, st));
-        g_launches += which == 0 ? ctx->k_first_res : which == 1 ? ctx->k_first : ctx->k_rest;
+        g_launches += which == 0 ? ctx->k_first_res[set] : which == 1 ? ctx->k_first[set]
+                                                             : ctx->k_rest[set];
         // keep the host-side roles in step with the replayed graph
         if (which < 2)
             for (Part& P : ctx->parts) std::swap(P.lev[0].lam, P.lev[0].lam2);
@@ -1593,8 +1611,10 @@ void wd_destroy(wd_ctx* ctx) {
     cudaDeviceSynchronize();   // no work of the context may still be in flight
     cudaGetLastError();
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
-    for (cudaGraphExec_t g : {ctx->g_first_res, ctx->g_first, ctx->g_rest, ctx->g_loop})
-        if (g) cudaGraphExecDestroy(g);
+    for (int v = 0; v < 2; v++)
+        for (cudaGraphExec_t g : {ctx->g_first_res[v], ctx->g_first[v], ctx->g_rest[v]})
+            if (g) cudaGraphExecDestroy(g);
+    if (ctx->g_loop) cudaGraphExecDestroy(ctx->g_loop);
     dfree(ctx->loopd);
     if (ctx->looph) cudaFreeHost(ctx->looph);
     if (ctx->cap) cudaStreamDestroy(ctx->cap);
@@ -2500,10 +2520,12 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
             if (!have) {   // first sweep of cycle c+1, returning the residual of lam_c
                 profile_first(ctx);    // the previous cycle's, before its events are reused
                 ctx->cyc_par ^= 1;
+                ctx->cyc_evented = c % PROF_EVERY == 0;
                 RC(run_split(ctx, 0, st));
+                ctx->prof[11] += 1;
                 RC(fetch_scalars(ctx, 1, st));
                 profile_rest(ctx);     // the previous cycle has finished
-                ctx->pend_first = true;
+                ctx->pend_first = ctx->cyc_evented;
                 ctx->pend_first_res = true;
                 first_done = true;
             }
@@ -2534,14 +2556,18 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
             if (!first_done) {
                 profile_first(ctx);
                 ctx->cyc_par ^= 1;
+                ctx->cyc_evented = c % PROF_EVERY == 0;
                 RC(run_split(ctx, 1, st));
-                ctx->pend_first = true;
+                ctx->prof[10] += 1;
+                ctx->pend_first = ctx->cyc_evented;
                 ctx->pend_first_res = false;
             }
             ctx->first_res = first_done;
             profile_rest(ctx);   // (already read: a no-op)
             RC(run_split(ctx, 2, st));
+            ctx->prof[10] += std::max(ctx->opt.pre_smooth + ctx->opt.post_smooth - 1, 0);
             ctx->pend_rest = ctx->opt.profile;
+            ctx->pend_rest_sweeps = ctx->cyc_evented;
             ctx->pend_par = ctx->cyc_par;
             c++;
             const double prev = c >= 2 ? ring4[(c - 2) & 3] : 0.0;
@@ -2582,7 +2608,7 @@ int wd_solve(wd_ctx* ctx, const double* f, const double* lambda0, double rel_tol
 // ------------------------------------------------------------------ profiling
 int wd_profile_read(const wd_ctx* ctx, double* out, int n) {
     if (!ctx || !out) return 0;
-    int m = n < 10 ? n : 10;
+    int m = n < 12 ? n : 12;
     for (int t = 0; t < m; t++) out[t] = ctx->prof[t];
     return m;
 }
