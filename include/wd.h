@@ -22,7 +22,8 @@
  * and the call then synchronises `stream` before returning.
  * `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
  * stream-ordered on it, except wd_assemble (synchronous) and wd_solve (which
- * synchronises once per V-cycle to test convergence).
+ * synchronises once per V-cycle to test convergence, or once per solve with
+ * wd_options.device_loop).
  *
  * Ownership: the caller owns every array passed in or out; the context owns
  * only internal copies and workspaces, allocated by wd_assemble and freed by
@@ -63,8 +64,9 @@ enum { WD_RULE_COUPLING_CUR = 0, WD_RULE_COUPLING_PAPER = 1, WD_RULE_VERBATIM = 
 /* Schedule of the 4-colour smoother.  Both compute the same
  * iterate bit for bit (same operations in the same order per node):
  *  FUSED   one launch per sweep: all four colour phases pipelined over k in
- *          shared-memory tiles (k_gs_fused.cu); on slab levels one 2-row halo
- *          exchange of lambda per sweep (default)
+ *          shared-memory tiles filled by TMA (k_gs_fused2.cu; k_gs_fused.cu for
+ *          levels of >= 2^31 entries); on slab levels one 2-row halo exchange
+ *          of lambda per sweep (default)
  *  PHASED  four launches per sweep, one per colour (k_mg.cu gs_phase_kernel);
  *          on slab levels halo rows exchanged after colours 1 and 3
  * and a different smoother (north_star "vertical-column line
